@@ -1,0 +1,204 @@
+/*
+ * grnnd_b200.h -- C ABI of libgrnnd_b200.so, the B200 (sm_100a) GRNND graph builder.
+ *
+ * Two layers, both plain pointers + sizes, no torch types:
+ *
+ *  (1) Kernel-module entry points.  One per function of the reference's
+ *      operator layer, the kernel module returned by grnnd.backend.get_kernels()
+ *      (/root/reference/pkg/src/grnnd/backend.py:58-64), with the same argument
+ *      meaning, the same in-place mutation of caller-owned arrays and the same
+ *      "no exceptions, status via flag" convention.  The
+ *      arrays are DEVICE pointers; paper_2510_02774_b200/kernels.py wraps them
+ *      in a numpy-in/numpy-out module with the reference's exact signatures.
+ *
+ *  (2) The fused round API used by paper_2510_02774_b200.build(): whole update /
+ *      reverse rounds as one asynchronous call each, on device-resident pools
+ *      (replaces builder.update_round / reverse_edge_sampling / finalize_graph,
+ *      /root/reference/pkg/src/grnnd/builder.py:283-362).
+ *
+ * Conventions: every function returns GRNND_OK (0) or an error code and never
+ * aborts; grnnd_last_error() describes the last failure on the calling thread.
+ * Calls are asynchronous on the given CUDA stream (NULL = legacy default
+ * stream); only functions documented as synchronising wait on the device.
+ * Device buffers belong to the caller (PyTorch tensors in the Python layer);
+ * the library never frees caller memory and keeps no device allocations of
+ * its own.  Ids are int32 with TOMBSTONE = -1 (core.py:22); distances are
+ * squared L2 in fp32, accumulated sequentially with separately rounded
+ * sub/mul/add exactly as the reference's _sqdist (_numba_kernels.py:50-56).
+ */
+#ifndef GRNND_B200_H
+#define GRNND_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GRNND_OK 0
+#define GRNND_EINVAL 1       /* bad argument (maps to ParamError in Python)        */
+#define GRNND_ECUDA 2        /* CUDA runtime / launch failure                        */
+#define GRNND_EUNSUPPORTED 3 /* shape outside what the kernels were built for        */
+#define GRNND_EWORKSPACE 4   /* workspace too small                                  */
+
+#define GRNND_TOMBSTONE (-1)
+#define GRNND_MAX_CAP 256 /* largest pool capacity R the kernels are compiled for */
+
+/* RoundStats fields (builder.py:102-114), device int64 counters */
+enum {
+    GRNND_ST_MESSAGES = 0,
+    GRNND_ST_REDIRECTS = 1,
+    GRNND_ST_SURVIVORS = 2,
+    GRNND_ST_REVERSE_ATTEMPTS = 3,
+    GRNND_ST_INSERTED = 4,
+    GRNND_ST_DUPLICATE = 5,
+    GRNND_ST_REPLACED = 6,
+    GRNND_ST_REJECTED = 7,
+    GRNND_ST_PAIRS = 8,     /* pair distances computed (all live pairs; instrumentation) */
+    GRNND_ST_PAIRS_REF = 9, /* pairs the reference loop would evaluate (instrumentation) */
+    GRNND_NSTATS = 16
+};
+
+typedef void *grnnd_stream_t; /* a cudaStream_t */
+
+const char *grnnd_last_error(void);
+int grnnd_abi_version(void);
+
+/* ------------------------------------------------------------------------ */
+/* (1) kernel-module entry points (device pointers)                          */
+/* ------------------------------------------------------------------------ */
+
+/* rng.hash4 / _numba_kernels.hash4_u64 (rng.py:34-41), elementwise over m (v, i) pairs */
+int grnnd_hash4_batch(uint64_t seed, uint64_t stream, const uint64_t *v, const uint64_t *i,
+                      int64_t m, uint64_t *out, grnnd_stream_t s);
+
+/* _numba_kernels.sqdist (:59-61): out[r] = sqdist(a[r,:], b[r,:]) for m row pairs */
+int grnnd_sqdist_batch(const float *a, const float *b, int64_t m, int32_t dim, float *out,
+                       grnnd_stream_t s);
+
+/* _numba_kernels.sample_initial (:91-115): out int32[n,count]; *fail_flag set to 1 on failure */
+int grnnd_sample_initial(int64_t n, int32_t count, uint64_t seed, int32_t *out,
+                         int64_t *fail_flag, grnnd_stream_t s);
+
+/* _numba_kernels.init_dists (:118-122): data fp32[n, ld] (first dim columns used) */
+int grnnd_init_dists(const float *data, int64_t n, int32_t dim, int32_t ld, const int32_t *ids,
+                     int32_t count, float *out, grnnd_stream_t s);
+
+/* Workspace the message-generating / grouping entry points need (bytes). */
+size_t grnnd_workspace_bytes(int64_t n, int32_t cap, int64_t msg_capacity);
+
+/* _numba_kernels.gen_update_messages (:125-192).  Writes per-vertex message
+ * slices (redirects in discovery order, then survivors in slot order) and
+ * tombstones redirected slots of read_ids in place. */
+int grnnd_gen_update_messages(const float *data, int64_t n, int32_t dim, int32_t ld,
+                              int32_t *read_ids, const float *read_dists,
+                              const int32_t *read_count, int32_t cap, uint64_t seed,
+                              uint64_t stream_id, int32_t order_code, int32_t *msg_tgt,
+                              int32_t *msg_id, float *msg_dist, int32_t *msg_cnt,
+                              void *workspace, size_t workspace_bytes, grnnd_stream_t s);
+
+/* _numba_kernels.gen_reverse_messages (:195-233) */
+int grnnd_gen_reverse_messages(const int32_t *read_ids, const float *read_dists,
+                               const int32_t *read_count, int64_t n, int32_t cap, double rho,
+                               int32_t *msg_tgt, int32_t *msg_id, float *msg_dist,
+                               int32_t *msg_cnt, grnnd_stream_t s);
+
+/* _numba_kernels.gen_merge_messages (:236-250) */
+int grnnd_gen_merge_messages(const int32_t *read_ids, const float *read_dists,
+                             const int32_t *read_count, int64_t n, int32_t cap, int32_t *msg_tgt,
+                             int32_t *msg_id, float *msg_dist, int32_t *msg_cnt,
+                             grnnd_stream_t s);
+
+/* build_flat step 1 (:265-270): offs int64[n+1] = exclusive prefix of msg_cnt (device). */
+int grnnd_message_offsets(const int32_t *msg_cnt, int64_t n, int64_t *offs, void *workspace,
+                          size_t workspace_bytes, grnnd_stream_t s);
+
+/* build_flat step 2 / _compact (:253-262): pack slices vertex-major using offs. */
+int grnnd_compact_messages(const int32_t *msg_tgt, const int32_t *msg_id, const float *msg_dist,
+                           const int32_t *msg_cnt, int64_t n, int32_t cap, const int64_t *offs,
+                           int32_t *flat_tgt, int32_t *flat_id, float *flat_dist,
+                           int32_t *flat_src, grnnd_stream_t s);
+
+/* group_by_target (:279-300): stable grouping; order int64[m], starts int64[n+1]. */
+int grnnd_group_by_target(const int32_t *flat_tgt, int64_t m, int64_t n, int64_t *order,
+                          int64_t *starts, void *workspace, size_t workspace_bytes,
+                          grnnd_stream_t s);
+
+/* apply_grouped_messages (:303-351).  outcomes: device int64[4] (ins, dup, rep, rej),
+ * accumulated (caller zeroes). */
+int grnnd_apply_grouped_messages(int32_t *write_ids, float *write_dists, int32_t *write_count,
+                                 int64_t n, int32_t cap, const int32_t *flat_id,
+                                 const float *flat_dist, const int64_t *order,
+                                 const int64_t *starts, int64_t *outcomes, grnnd_stream_t s);
+
+/* ------------------------------------------------------------------------ */
+/* (2) fused round API on device-resident double-buffered pools              */
+/* ------------------------------------------------------------------------ */
+
+typedef struct {
+    const float *data; /* fp32 [n_total, ld], replicated on every rank                     */
+    int64_t n_total;   /* global vertex count                                              */
+    int64_t lo, hi;    /* owned vertex range [lo, hi) (0, n_total on one GPU)              */
+    int32_t dim, ld, cap;
+    int32_t *read_ids; /* int32 [hi-lo, cap]   row r = vertex lo + r                       */
+    float *read_dists; /* fp32  [hi-lo, cap]                                               */
+    int32_t *read_count;
+    int32_t *write_ids;
+    float *write_dists;
+    int32_t *write_count;
+    void *workspace;   /* >= grnnd_workspace_bytes(hi-lo, cap, msg_capacity)               */
+    size_t workspace_bytes;
+    int64_t msg_capacity; /* messages one round may emit / receive on this rank             */
+    int64_t *stats;    /* device int64 [GRNND_NSTATS], accumulated by the round calls      */
+} grnnd_pools;
+
+/* builder.init_neighbors (:221-257): sample S ids, their distances, count = S.
+ * fail_flag: device int64[1]. */
+int grnnd_init_pools(const grnnd_pools *p, int32_t S, uint64_t seed, int64_t *fail_flag,
+                     grnnd_stream_t s);
+
+/* builder.update_round (:283-312) minus the buffer swap (the caller swaps pointers).
+ * One GPU: everything on device, asynchronous. */
+int grnnd_update_round(const grnnd_pools *p, uint64_t seed, uint64_t stream_id,
+                       int32_t order_code, grnnd_stream_t s);
+
+/* builder.reverse_edge_sampling (:315-339) minus the swap. */
+int grnnd_reverse_round(const grnnd_pools *p, double rho, grnnd_stream_t s);
+
+/* Multi-GPU split of a round.  emit: pair phase (or reverse selection) of owned
+ * vertices into the outgoing message list, bucketed by owner rank.  The host then
+ * exchanges the buckets (NCCL all-to-all) into the incoming list and calls
+ * grnnd_round_apply. See paper_2510_02774_b200/sharded.py. */
+int grnnd_round_emit(const grnnd_pools *p, int32_t kind /*0 update, 1 reverse*/, uint64_t seed,
+                     uint64_t stream_id, int32_t order_code, double rho,
+                     const int64_t *rank_bounds /*device int64[nranks+1]*/, int32_t nranks,
+                     int64_t *send_counts /*device int64[nranks]*/, grnnd_stream_t s);
+/* device pointers to the outgoing (bucketed by rank) and incoming message arrays inside
+ * the workspace: key int64, tgt int32, id int32, dist fp32 */
+int grnnd_round_buffers(const grnnd_pools *p, int64_t **out_key, int32_t **out_tgt,
+                        int32_t **out_id, float **out_dist, int64_t **in_key, int32_t **in_tgt,
+                        int32_t **in_id, float **in_dist);
+int grnnd_round_apply(const grnnd_pools *p, int32_t kind, int64_t n_incoming, grnnd_stream_t s);
+
+/* builder.finalize_graph (:342-362): rows sorted by (dist, id) into CSR.
+ * offsets int64[n+1] (device), nbrs int32[sum(counts)] (device).  The Graph.validate
+ * checks of core.py:171-201 run in the same pass: *bad_flag (device int64, nullable)
+ * gets bit 0 = id out of range, bit 1 = self loop, bit 2 = duplicate within a row. */
+int grnnd_finalize(const int32_t *ids, const float *dists, const int32_t *counts, int64_t n,
+                   int32_t cap, int64_t *offsets, int32_t *nbrs, int64_t *bad_flag,
+                   void *workspace, size_t workspace_bytes, grnnd_stream_t s);
+
+/* Dataset.validate finiteness scan (core.py:70-71) on device: *bad_flag = 1 if any of the
+ * first dim columns of data[n, ld] is NaN/inf. */
+int grnnd_check_finite(const float *data, int64_t n, int32_t dim, int32_t ld, int64_t *bad_flag,
+                       grnnd_stream_t s);
+
+/* Row-sorted fixed-degree view (the fixed-degree int32 [n, cap] adjacency, -1 padded). */
+int grnnd_sorted_rows(const int32_t *ids, const float *dists, const int32_t *counts, int64_t n,
+                      int32_t cap, int32_t *out_ids, grnnd_stream_t s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRNND_B200_H */

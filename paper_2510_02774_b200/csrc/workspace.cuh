@@ -1,0 +1,87 @@
+// workspace.cuh -- carving of the caller-provided workspace (device bytes) into the
+// per-round scratch the kernels use.  The library never allocates device memory.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+namespace grnnd {
+
+constexpr int NBINS = 6;  // propagate bins by live count k: see propagate.cu
+constexpr int HEAVY_SEG = 32;  // segments longer than this are sorted by a CTA
+
+// small counters block (unsigned long long so atomicAdd works on it)
+enum Counter : int {
+    C_LIST = 0,          // messages appended to the emit list this round
+    C_BIN0 = 1,          // C_BIN0 + b: vertices in propagate bin b
+    C_HEAVY = C_BIN0 + NBINS,  // segments with > HEAVY_SEG entries
+    C_OVERFLOW,          // set when the emit list would exceed msg_capacity
+    C_NCOUNTERS = 16
+};
+
+struct Workspace {
+    unsigned long long *ctr;  // [C_NCOUNTERS]
+    // emit list (message order irrelevant: the key carries the global order)
+    int64_t *e_key;
+    int32_t *e_tgt;
+    int32_t *e_id;
+    float *e_dist;
+    // rank-bucketed copy (multi-GPU send buffer) -- also scratch for huge segment sorts
+    int64_t *o_key;
+    int32_t *o_tgt;
+    int32_t *o_id;
+    float *o_dist;
+    // inbox grouped by target row
+    int64_t *i_key;
+    int32_t *i_id;
+    float *i_dist;
+    int32_t *in_count;   // [n+1] per-target counts (self-resetting)
+    int64_t *starts;     // [n+1]
+    int64_t *scan_tmp;   // [scan blocks + 1]
+    int32_t *bins;       // [n] vertex lists, bin b at bins + bin_off[b] ... (packed by counts)
+    int32_t *heavy;      // [n] heavy segment ids
+    int64_t n;
+    int64_t msg_capacity;
+};
+
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+constexpr int SCAN_ITEMS = 2048;  // elements per scan block
+
+inline int64_t scan_blocks(int64_t n) { return (n + SCAN_ITEMS - 1) / SCAN_ITEMS; }
+
+// Layout: computes offsets; with base == nullptr returns the byte size only.
+inline size_t carve(Workspace *w, void *base, int64_t n, int64_t msg_capacity) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) -> void * {
+        off = align_up(off, 256);
+        void *p = base ? (void *)((char *)base + off) : nullptr;
+        off += bytes;
+        return p;
+    };
+    const size_t C = (size_t)(msg_capacity > 0 ? msg_capacity : 1);
+    const size_t N = (size_t)(n > 0 ? n : 1);
+    Workspace t;
+    t.ctr = (unsigned long long *)take(sizeof(unsigned long long) * C_NCOUNTERS);
+    t.e_key = (int64_t *)take(8 * C);
+    t.e_tgt = (int32_t *)take(4 * C);
+    t.e_id = (int32_t *)take(4 * C);
+    t.e_dist = (float *)take(4 * C);
+    t.o_key = (int64_t *)take(8 * C);
+    t.o_tgt = (int32_t *)take(4 * C);
+    t.o_id = (int32_t *)take(4 * C);
+    t.o_dist = (float *)take(4 * C);
+    t.i_key = (int64_t *)take(8 * C);
+    t.i_id = (int32_t *)take(4 * C);
+    t.i_dist = (float *)take(4 * C);
+    t.in_count = (int32_t *)take(4 * (N + 1));
+    t.starts = (int64_t *)take(8 * (N + 1));
+    t.scan_tmp = (int64_t *)take(8 * (size_t)(scan_blocks((int64_t)N) + 2 + 128));
+    t.bins = (int32_t *)take(4 * N * NBINS);
+    t.heavy = (int32_t *)take(4 * N);
+    t.n = n;
+    t.msg_capacity = msg_capacity;
+    if (w) *w = t;
+    return align_up(off, 256);
+}
+
+}  // namespace grnnd

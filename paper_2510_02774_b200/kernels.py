@@ -1,0 +1,230 @@
+"""The reference's kernel-module interface, served by the B200 kernels.
+
+``grnnd.backend.get_kernels()`` returns a module with a fixed function set
+(/root/reference/pkg/src/grnnd/backend.py:58-64; functions in
+_numba_kernels.py:44-351).  This module implements the build-path subset with
+the same names, argument meaning, numpy-in / numpy-out calling convention and
+in-place mutation of caller-owned arrays, so the reference's builder (or its
+tests) can run on the GPU kernels unchanged -- see INTEGRATION.md for the
+one-line backend hook.  Each call stages its arrays to the device, runs the
+sm_100a kernel through the C ABI, and copies the results back; it is the
+parity surface, not the fast path (``paper_2510_02774_b200.build`` keeps the
+pools resident in HBM instead).
+
+Evaluation kernels (brute_force, greedy_search_*, refine_accept_loop) are out
+of scope for this build-path drop-in and raise NotImplementedError.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .builder import _device, _stream, padded_ld, upload
+
+TOMB = np.int32(-1)
+ORDER_DISORDERED = 0
+ORDER_ASCENDING = 1
+_M64 = (1 << 64) - 1
+
+
+def _dev():
+    return _device(None)
+
+
+def _to(a: np.ndarray, dtype) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=dtype)).to(_dev())
+
+
+def _ws(n: int, cap: int, mcap: int) -> torch.Tensor:
+    return torch.zeros(int(_lib.lib.grnnd_workspace_bytes(n, cap, mcap)), dtype=torch.uint8, device=_dev())
+
+
+def _writeback_slices(dst: np.ndarray, src: torch.Tensor, cnt: np.ndarray, cap: int) -> None:
+    """Copy only the [0, cnt[v]) prefix of each width-cap slice (untouched tail kept)."""
+    s = src.cpu().numpy()
+    mask = (np.arange(cap)[None, :] < cnt[:, None]).ravel()
+    dst[mask] = s[mask]
+
+
+def hash4_u64(seed, stream, v, i):
+    """_numba_kernels.hash4_u64 (:44-47)."""
+    dev = _dev()
+    bits = np.array([int(v) & _M64, int(i) & _M64], dtype=np.uint64).view(np.int64)
+    vi = torch.from_numpy(bits).to(dev)  # u64 bit patterns carried in int64 storage
+    out = torch.empty(1, dtype=torch.int64, device=dev)
+    _lib.call("grnnd_hash4_batch", int(seed) & _M64, int(stream) & _M64, vi.data_ptr(), vi.data_ptr() + 8, 1,
+              out.data_ptr(), _stream(dev))
+    return np.uint64(out.cpu().numpy().view(np.uint64)[0])
+
+
+def sqdist(a, b):
+    """_numba_kernels.sqdist (:59-61): exact sequential fp32 squared distance."""
+    dev = _dev()
+    ta, tb = _to(np.asarray(a).reshape(1, -1), np.float32), _to(np.asarray(b).reshape(1, -1), np.float32)
+    out = torch.empty(1, dtype=torch.float32, device=dev)
+    _lib.call("grnnd_sqdist_batch", ta.data_ptr(), tb.data_ptr(), 1, ta.shape[1], out.data_ptr(), _stream(dev))
+    return np.float32(out.item())
+
+
+def sample_initial(n, count, seed, out, fail_flag):
+    """_numba_kernels.sample_initial (:91-115); fills ``out`` and ``fail_flag`` in place."""
+    dev = _dev()
+    t = torch.full((int(n), int(count)), -1, dtype=torch.int32, device=dev)
+    f = torch.zeros(1, dtype=torch.int64, device=dev)
+    _lib.call("grnnd_sample_initial", int(n), int(count), int(seed) & _M64, t.data_ptr(), f.data_ptr(), _stream(dev))
+    out[...] = t.cpu().numpy()
+    if int(f.item()):
+        fail_flag[0] = 1
+
+
+def init_dists(data, ids, out):
+    """_numba_kernels.init_dists (:118-122)."""
+    dev = _dev()
+    d = upload(np.asarray(data), dev)
+    ti = _to(ids, np.int32)
+    to = torch.empty(ti.shape, dtype=torch.float32, device=dev)
+    _lib.call("grnnd_init_dists", d.data_ptr(), d.shape[0], data.shape[1], d.shape[1], ti.data_ptr(), ti.shape[1],
+              to.data_ptr(), _stream(dev))
+    out[...] = to.cpu().numpy()
+
+
+def gen_update_messages(data, read_ids, read_dists, read_count, seed, stream, order_code,
+                        msg_tgt, msg_id, msg_dist, msg_cnt):
+    """_numba_kernels.gen_update_messages (:125-192); mutates read_ids (tombstones),
+    msg_* slices and msg_cnt in place."""
+    dev = _dev()
+    n, cap = read_ids.shape
+    d = upload(np.asarray(data), dev)
+    ri = _to(read_ids, np.int32)
+    rd = _to(read_dists, np.float32)
+    rc = _to(read_count, np.int32)
+    mt = torch.empty(n * cap, dtype=torch.int32, device=dev)
+    mi = torch.empty(n * cap, dtype=torch.int32, device=dev)
+    md = torch.empty(n * cap, dtype=torch.float32, device=dev)
+    mc = torch.zeros(n, dtype=torch.int32, device=dev)
+    ws = _ws(n, cap, 0)
+    _lib.call("grnnd_gen_update_messages", d.data_ptr(), n, data.shape[1], d.shape[1], ri.data_ptr(), rd.data_ptr(),
+              rc.data_ptr(), cap, int(seed) & _M64, int(stream) & _M64, int(order_code), mt.data_ptr(), mi.data_ptr(),
+              md.data_ptr(), mc.data_ptr(), ws.data_ptr(), ws.numel(), _stream(dev))
+    cnt = mc.cpu().numpy()
+    msg_cnt[...] = cnt
+    read_ids[...] = ri.cpu().numpy()
+    _writeback_slices(msg_tgt, mt, cnt, cap)
+    _writeback_slices(msg_id, mi, cnt, cap)
+    _writeback_slices(msg_dist, md, cnt, cap)
+
+
+def _reverse_like(fn, read_ids, read_dists, read_count, extra, msg_tgt, msg_id, msg_dist, msg_cnt):
+    dev = _dev()
+    n, cap = read_ids.shape
+    ri, rd, rc = _to(read_ids, np.int32), _to(read_dists, np.float32), _to(read_count, np.int32)
+    mt = torch.empty(n * cap, dtype=torch.int32, device=dev)
+    mi = torch.empty(n * cap, dtype=torch.int32, device=dev)
+    md = torch.empty(n * cap, dtype=torch.float32, device=dev)
+    mc = torch.zeros(n, dtype=torch.int32, device=dev)
+    _lib.call(fn, ri.data_ptr(), rd.data_ptr(), rc.data_ptr(), n, cap, *extra, mt.data_ptr(), mi.data_ptr(),
+              md.data_ptr(), mc.data_ptr(), _stream(dev))
+    cnt = mc.cpu().numpy()
+    msg_cnt[...] = cnt
+    _writeback_slices(msg_tgt, mt, cnt, cap)
+    _writeback_slices(msg_id, mi, cnt, cap)
+    _writeback_slices(msg_dist, md, cnt, cap)
+
+
+def gen_reverse_messages(read_ids, read_dists, read_count, rho, msg_tgt, msg_id, msg_dist, msg_cnt):
+    """_numba_kernels.gen_reverse_messages (:195-233)."""
+    _reverse_like("grnnd_gen_reverse_messages", read_ids, read_dists, read_count, (float(rho),),
+                  msg_tgt, msg_id, msg_dist, msg_cnt)
+
+
+def gen_merge_messages(read_ids, read_dists, read_count, msg_tgt, msg_id, msg_dist, msg_cnt):
+    """_numba_kernels.gen_merge_messages (:236-250)."""
+    _reverse_like("grnnd_gen_merge_messages", read_ids, read_dists, read_count, (),
+                  msg_tgt, msg_id, msg_dist, msg_cnt)
+
+
+def build_flat(msg_tgt, msg_id, msg_dist, msg_cnt, cap):
+    """_numba_kernels.build_flat (:265-276): vertex-major flat (tgt, id, dist, src)."""
+    dev = _dev()
+    n = msg_cnt.shape[0]
+    mc = _to(msg_cnt, np.int32)
+    offs = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    ws = _ws(n, int(cap), 0)
+    _lib.call("grnnd_message_offsets", mc.data_ptr(), n, offs.data_ptr(), ws.data_ptr(), ws.numel(), _stream(dev))
+    total = int(offs[-1].item())
+    mt, mi, md = _to(msg_tgt, np.int32), _to(msg_id, np.int32), _to(msg_dist, np.float32)
+    ft = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    fi = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    fd = torch.empty(max(total, 1), dtype=torch.float32, device=dev)
+    fs = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    _lib.call("grnnd_compact_messages", mt.data_ptr(), mi.data_ptr(), md.data_ptr(), mc.data_ptr(), n, int(cap),
+              offs.data_ptr(), ft.data_ptr(), fi.data_ptr(), fd.data_ptr(), fs.data_ptr(), _stream(dev))
+    return (ft[:total].cpu().numpy(), fi[:total].cpu().numpy(), fd[:total].cpu().numpy(),
+            fs[:total].cpu().numpy())
+
+
+def group_by_target(flat_tgt, n):
+    """_numba_kernels.group_by_target (:294-300): stable grouping -> (order int64, starts int64)."""
+    dev = _dev()
+    m = int(flat_tgt.shape[0])
+    ft = _to(flat_tgt if m else np.zeros(1, np.int32), np.int32)
+    order = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
+    starts = torch.empty(int(n) + 1, dtype=torch.int64, device=dev)
+    ws = _ws(int(n), 1, max(m, 1))
+    _lib.call("grnnd_group_by_target", ft.data_ptr(), m, int(n), order.data_ptr(), starts.data_ptr(),
+              ws.data_ptr(), ws.numel(), _stream(dev))
+    return order[:m].cpu().numpy(), starts.cpu().numpy()
+
+
+def apply_grouped_messages(write_ids, write_dists, write_count, flat_id, flat_dist, grp_order, grp_start):
+    """_numba_kernels.apply_grouped_messages (:303-351); mutates the write buffers,
+    returns (inserted, duplicate, replaced, rejected)."""
+    dev = _dev()
+    n, cap = write_ids.shape
+    wi, wd, wc = _to(write_ids, np.int32), _to(write_dists, np.float32), _to(write_count, np.int32)
+    m = len(flat_id)
+    fi = _to(flat_id if m else np.zeros(1, np.int32), np.int32)
+    fd = _to(flat_dist if m else np.zeros(1, np.float32), np.float32)
+    od = _to(grp_order if len(grp_order) else np.zeros(1, np.int64), np.int64)
+    st = _to(grp_start, np.int64)
+    oc = torch.zeros(4, dtype=torch.int64, device=dev)
+    _lib.call("grnnd_apply_grouped_messages", wi.data_ptr(), wd.data_ptr(), wc.data_ptr(), n, cap, fi.data_ptr(),
+              fd.data_ptr(), od.data_ptr(), st.data_ptr(), oc.data_ptr(), _stream(dev))
+    write_ids[...] = wi.cpu().numpy()
+    write_dists[...] = wd.cpu().numpy()
+    write_count[...] = wc.cpu().numpy()
+    ins, dup, rep, rej = (int(x) for x in oc.cpu().numpy())
+    return ins, dup, rep, rej
+
+
+def warmup() -> None:
+    """Load the library and touch every build-path entry point once."""
+    data = np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0], [1.0, 1.0]], dtype=np.float32)
+    ids = np.full((4, 1), -1, np.int32)
+    flag = np.zeros(1, np.int64)
+    sample_initial(4, 1, 1, ids, flag)
+    dists = np.zeros((4, 1), np.float32)
+    init_dists(data, ids, dists)
+    hash4_u64(1, 2, 3, 4)
+    sqdist(data[0], data[1])
+
+
+def _out_of_scope(name):
+    def f(*a, **k):
+        raise NotImplementedError(f"{name} is an evaluation kernel, outside the B200 build-path drop-in")
+    f.__name__ = name
+    return f
+
+
+brute_force = _out_of_scope("brute_force")
+greedy_search_single = _out_of_scope("greedy_search_single")
+greedy_search_batch = _out_of_scope("greedy_search_batch")
+refine_accept_loop = _out_of_scope("refine_accept_loop")
+
+__all__ = [
+    "hash4_u64", "sqdist", "sample_initial", "init_dists", "gen_update_messages", "gen_reverse_messages",
+    "gen_merge_messages", "build_flat", "group_by_target", "apply_grouped_messages", "warmup",
+    "padded_ld",
+]
