@@ -64,6 +64,8 @@ typedef void *grnnd_stream_t; /* a cudaStream_t */
 
 const char *grnnd_last_error(void);
 int grnnd_abi_version(void);
+/* kernels launched by this library since load (host-side counter; for launch accounting) */
+unsigned long long grnnd_launch_count(void);
 
 /* ------------------------------------------------------------------------ */
 /* (1) kernel-module entry points (device pointers)                          */
@@ -165,6 +167,14 @@ int grnnd_update_round(const grnnd_pools *p, uint64_t seed, uint64_t stream_id,
 
 /* builder.reverse_edge_sampling (:315-339) minus the swap. */
 int grnnd_reverse_round(const grnnd_pools *p, double rho, grnnd_stream_t s);
+
+/* The two halves of a round, for per-phase timing: emit (pair phase / reverse selection
+ * into the message list) then apply (group by target + pool insert).  update_round ==
+ * update_emit + apply_emitted(kind 0); reverse_round == reverse_emit + apply_emitted(1). */
+int grnnd_update_emit(const grnnd_pools *p, uint64_t seed, uint64_t stream_id,
+                      int32_t order_code, grnnd_stream_t s);
+int grnnd_reverse_emit(const grnnd_pools *p, double rho, grnnd_stream_t s);
+int grnnd_apply_emitted(const grnnd_pools *p, int32_t kind, grnnd_stream_t s);
 
 /* Multi-GPU split of a round.  emit: pair phase (or reverse selection) of owned
  * vertices into the outgoing message list, bucketed by owner rank.  The host then

@@ -56,6 +56,10 @@ class Pools(C.Structure):
 _SIGS = {
     "grnnd_last_error": (C.c_char_p, []),
     "grnnd_abi_version": (C.c_int, []),
+    "grnnd_launch_count": (C.c_ulonglong, []),
+    "grnnd_update_emit": (C.c_int, [C.POINTER(Pools), _u64, _u64, _i32, _vp]),
+    "grnnd_reverse_emit": (C.c_int, [C.POINTER(Pools), _dbl, _vp]),
+    "grnnd_apply_emitted": (C.c_int, [C.POINTER(Pools), _i32, _vp]),
     "grnnd_hash4_batch": (C.c_int, [_u64, _u64, _vp, _vp, _i64, _vp, _vp]),
     "grnnd_sqdist_batch": (C.c_int, [_vp, _vp, _i64, _i32, _vp, _vp]),
     "grnnd_sample_initial": (C.c_int, [_i64, _i32, _u64, _vp, _vp, _vp]),

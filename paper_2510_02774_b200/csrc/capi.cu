@@ -17,7 +17,12 @@ void set_error(const char *fmt, ...) {
     va_end(ap);
 }
 
-int check_launch(const char *what) {
+static unsigned long long g_launches = 0;  // kernels this library launched (host-side count)
+
+unsigned long long launch_count() { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
+int check_launch(const char *what, int nkernels) {
+    __atomic_fetch_add(&g_launches, (unsigned long long)nkernels, __ATOMIC_RELAXED);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         set_error("%s: %s", what, cudaGetErrorString(e));
@@ -29,12 +34,12 @@ int check_launch(const char *what) {
 static inline cudaStream_t S(grnnd_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
 static int check_ws(void *ws, size_t bytes, int64_t n, int32_t cap, int64_t mcap, Workspace *w) {
-    const size_t need = carve(nullptr, nullptr, n, mcap);
+    const size_t need = carve(nullptr, nullptr, n, cap, mcap);
     if (!ws || bytes < need) {
         set_error("workspace too small: %zu < %zu bytes", bytes, need);
         return GRNND_EWORKSPACE;
     }
-    carve(w, ws, n, mcap);
+    carve(w, ws, n, cap, mcap);
     return GRNND_OK;
 }
 
@@ -96,6 +101,7 @@ extern "C" {
 
 const char *grnnd_last_error(void) { return g_err; }
 int grnnd_abi_version(void) { return 1; }
+unsigned long long grnnd_launch_count(void) { return launch_count(); }
 
 int grnnd_hash4_batch(uint64_t seed, uint64_t stream, const uint64_t *v, const uint64_t *i, int64_t m, uint64_t *out,
                       grnnd_stream_t s) {
@@ -133,8 +139,7 @@ int grnnd_init_dists(const float *data, int64_t n, int32_t dim, int32_t ld, cons
 }
 
 size_t grnnd_workspace_bytes(int64_t n, int32_t cap, int64_t msg_capacity) {
-    (void)cap;
-    return carve(nullptr, nullptr, n, msg_capacity);
+    return carve(nullptr, nullptr, n, cap, msg_capacity);
 }
 
 int grnnd_gen_update_messages(const float *data, int64_t n, int32_t dim, int32_t ld, int32_t *read_ids,
@@ -281,7 +286,7 @@ int grnnd_init_pools(const grnnd_pools *p, int32_t S_, uint64_t seed, int64_t *f
     if (n > 0) {
         fill_i32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, S(s)>>>(p->read_count, n, S_);
         fill_i32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, S(s)>>>(p->write_count, n, 0);
-        GRNND_TRY(check_launch("fill_counts"));
+        GRNND_TRY(check_launch("fill_counts", 2));
     }
     GRNND_CUDA(cudaMemsetAsync(w.ctr, 0, sizeof(unsigned long long) * C_NCOUNTERS, S(s)));
     return GRNND_OK;
@@ -366,6 +371,35 @@ int grnnd_reverse_round(const grnnd_pools *p, double rho, grnnd_stream_t s) {
     GRNND_CUDA(cudaMemsetAsync(w.ctr + C_LIST, 0, sizeof(unsigned long long), S(s)));
     GRNND_TRY(emit_reverse(p, w, rho, S(s)));
     return apply_phase(p, w, 1, w.ctr + C_LIST, p->msg_capacity, S(s));
+}
+
+int grnnd_update_emit(const grnnd_pools *p, uint64_t seed, uint64_t stream_id, int32_t order_code,
+                      grnnd_stream_t s) {
+    Workspace w;
+    GRNND_TRY(pools_workspace(p, &w));
+    if (order_code != 0 && order_code != 1) {
+        set_error("order_code must be 0 or 1");
+        return GRNND_EINVAL;
+    }
+    GRNND_CUDA(cudaMemsetAsync(w.ctr + C_LIST, 0, sizeof(unsigned long long), S(s)));
+    return emit_update(p, w, seed, stream_id, order_code, S(s));
+}
+
+int grnnd_reverse_emit(const grnnd_pools *p, double rho, grnnd_stream_t s) {
+    Workspace w;
+    GRNND_TRY(pools_workspace(p, &w));
+    if (!(rho > 0.0 && rho <= 1.0)) {
+        set_error("rho must be in (0, 1]");
+        return GRNND_EINVAL;
+    }
+    GRNND_CUDA(cudaMemsetAsync(w.ctr + C_LIST, 0, sizeof(unsigned long long), S(s)));
+    return emit_reverse(p, w, rho, S(s));
+}
+
+int grnnd_apply_emitted(const grnnd_pools *p, int32_t kind, grnnd_stream_t s) {
+    Workspace w;
+    GRNND_TRY(pools_workspace(p, &w));
+    return apply_phase(p, w, kind, w.ctr + C_LIST, p->msg_capacity, S(s));
 }
 
 int grnnd_round_emit(const grnnd_pools *p, int32_t kind, uint64_t seed, uint64_t stream_id, int32_t order_code,

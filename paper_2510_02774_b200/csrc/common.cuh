@@ -86,7 +86,8 @@ __device__ __forceinline__ T warp_sum(T v) {
 // ---- host-side error plumbing (capi.cu) ----
 namespace grnnd {
 void set_error(const char* fmt, ...);
-int check_launch(const char* what);
+int check_launch(const char* what, int nkernels = 1);
+unsigned long long launch_count();
 }  // namespace grnnd
 
 #define GRNND_TRY(expr)                        \

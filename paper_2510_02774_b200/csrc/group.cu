@@ -111,7 +111,7 @@ static int scan_impl(const int32_t *counts, int64_t n, int64_t *out, int64_t *tm
     scan_reduce_kernel<<<(unsigned)nb, SCAN_T, 0, st>>>(counts, n, tmp);
     scan_top_kernel<<<1, 1024, 0, st>>>(tmp, nb);
     scan_down_kernel<<<(unsigned)nb, SCAN_T, 0, st>>>(counts, n, tmp, out, nb, heavy_ctr, heavy_list);
-    return check_launch("scan");
+    return check_launch("scan", 3);
 }
 
 int launch_scan_counts(const int32_t *counts, int64_t n, int64_t *out, int64_t *tmp, cudaStream_t st) {
@@ -418,7 +418,7 @@ int launch_bucket_by_rank(const Workspace &w, const int64_t *rank_bounds, int32_
     rank_count_kernel<<<g, 256, 0, st>>>(w, rank_bounds, nranks, rc);
     rank_offsets_kernel<<<1, 32, 0, st>>>(rc, nranks, cursor, send_counts);
     rank_scatter_kernel<<<g, 256, 0, st>>>(w, rank_bounds, nranks, cursor);
-    return check_launch("bucket_by_rank");
+    return check_launch("bucket_by_rank", 3);
 }
 
 }  // namespace grnnd

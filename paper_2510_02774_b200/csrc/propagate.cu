@@ -7,18 +7,21 @@
 // member toward the closer one (tombstoning it); survivors stay.
 //
 // B200 design:
-//  * vertices are binned by k; each bin runs a persistent kernel whose CTA processes
-//    one vertex at a time with a CTA size / shared-memory slab matched to the bin;
+//  * bin_kernel (thread per vertex) bins vertices by k and computes each vertex's
+//    Fisher-Yates permutation off the critical path (positions stored as bytes);
+//  * each bin runs a persistent kernel whose CTA processes one vertex at a time with a
+//    CTA size / shared-memory slab matched to the bin;
 //  * the k pool rows are gathered HBM -> smem with cp.async (16 B, L2-only), row-major
 //    with a 16-byte XOR swizzle so the register-tiled reads below are conflict free;
 //  * ALL pair distances of the pool (upper triangle, slot order) are computed with
 //    4x4 register tiles in the reference's exact arithmetic (sequential fp32
 //    sub/mul/add, no FMA) -> bit-identical distances to the numba oracle;
-//  * the order-dependent part (anchor-serial rule, SURVEY 7 hard part 1) is then a
-//    cheap pass over 64-bit masks: cond[x] (pair redirects) and afar[x] (anchor is the
-//    farther one), both indexed by permutation position;
-//  * emitted messages get their distance re-evaluated exactly from L2-resident rows
-//    (only ~10% of entries are redirected), keeping the big distance matrix out of smem.
+//  * the order-dependent part (anchor-serial rule, SURVEY 7 hard part 1) is a
+//    warp-parallel scan over 64-bit masks: cond[x] (pair redirects) and afar[x] (anchor
+//    is the farther member), indexed by permutation position; __ballot finds the next
+//    anchor that still has a live redirect partner, so anchors without one cost nothing;
+//  * emitted redirects get their distance re-evaluated exactly from the smem rows
+//    (or L2 for D > 128), keeping the k x k distance matrix out of shared memory.
 #include <cstdio>
 
 #include "common.cuh"
@@ -26,10 +29,6 @@
 
 namespace grnnd {
 
-// bin b covers k in (BIN_HI[b-1], BIN_HI[b]]; bin 0 = k <= 1 (no pairs)
-__host__ __device__ constexpr int bin_hi(int b) {
-    return b == 0 ? 1 : b == 1 ? 16 : b == 2 ? 32 : b == 3 ? 64 : b == 4 ? 128 : 256;
-}
 __device__ __forceinline__ int bin_of(int k) {
     return k <= 1 ? 0 : k <= 16 ? 1 : k <= 32 ? 2 : k <= 64 ? 3 : k <= 128 ? 4 : 5;
 }
@@ -37,30 +36,50 @@ __device__ __forceinline__ int bin_of(int k) {
 constexpr int DC4 = 32;  // float4 per row chunk (128 dims)
 
 // ---------------------------------------------------------------------------------
-// binning: one pass over read_count; bin lists + sum(k) into stats
+// binning + per-vertex Fisher-Yates permutation (_fill_perm :64-74), thread per vertex
 // ---------------------------------------------------------------------------------
-__global__ void bin_kernel(const int32_t *__restrict__ read_count, int64_t n, int32_t cap,
-                           Workspace w, int64_t *__restrict__ stats, int slice_mode,
-                           const int32_t *__restrict__ read_ids,
-                           const float *__restrict__ read_dists, int64_t lo,
-                           int32_t *__restrict__ msg_tgt, int32_t *__restrict__ msg_id,
+__device__ __forceinline__ uint32_t mod_small(uint64_t h, uint32_t m) {
+    // h % m for m < 2^16 with 32-bit remainders only: h = hi * 2^32 + lo
+    const uint32_t hi = (uint32_t)(h >> 32), lo = (uint32_t)h;
+    const uint32_t r32 = (0xFFFFFFFFu % m + 1u) % m;  // 2^32 mod m in 32-bit arithmetic
+    return (uint32_t)(((uint64_t)(hi % m) * r32 + (lo % m)) % m);
+}
+
+__global__ void bin_kernel(const int32_t *__restrict__ read_count, int64_t n, int32_t cap, Workspace w,
+                           int64_t *__restrict__ stats, int slice_mode, const int32_t *__restrict__ read_ids,
+                           const float *__restrict__ read_dists, int64_t lo, uint64_t seed, uint64_t stream_id,
+                           int order_code, int32_t *__restrict__ msg_tgt, int32_t *__restrict__ msg_id,
                            float *__restrict__ msg_dist, int32_t *__restrict__ msg_cnt) {
     __shared__ unsigned long long s_sum;
     if (threadIdx.x == 0) s_sum = 0;
     __syncthreads();
-    int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int k = 0;
     if (v < n) {
         k = read_count[v];
-        int b = bin_of(k);
+        const int b = bin_of(k);
         if (b > 0) {
-            unsigned peers = __match_any_sync(__activemask(), b);
-            int leader = __ffs(peers) - 1;
+            const unsigned peers = __match_any_sync(__activemask(), b);
+            const int leader = __ffs(peers) - 1;
             unsigned long long base = 0;
             if (lane_id() == leader) base = atomicAdd(&w.ctr[C_BIN0 + b], (unsigned long long)__popc(peers));
             base = __shfl_sync(peers, base, leader);
-            int rank = __popc(peers & ((1u << lane_id()) - 1));
+            const int rank = __popc(peers & ((1u << lane_id()) - 1));
             w.bins[(int64_t)b * w.n + (int64_t)base + rank] = (int32_t)v;
+            if (order_code == 0) {
+                // perm = identity; for i = k-1..1: swap(perm[i], perm[hash4(seed,stream,v,i) % (i+1)])
+                uint8_t perm[GRNND_MAX_CAP];
+                for (int i = 0; i < k; ++i) perm[i] = (uint8_t)i;
+                const uint64_t pre = vertex_prefix(seed, stream_id, (uint64_t)(lo + v));
+                for (int i = k - 1; i > 0; --i) {
+                    const int j = (int)mod_small(mix64(pre ^ (uint64_t)i), (uint32_t)(i + 1));
+                    const uint8_t t = perm[i];
+                    perm[i] = perm[j];
+                    perm[j] = t;
+                }
+                uint8_t *pos = w.pos8 + v * cap;
+                for (int x = 0; x < k; ++x) pos[perm[x]] = (uint8_t)x;
+            }
         } else if (slice_mode) {
             // k <= 1: no pairs; the lone live entry (if any) survives (:186-192)
             int c = 0;
@@ -84,16 +103,19 @@ __global__ void bin_kernel(const int32_t *__restrict__ read_count, int64_t n, in
 // the pair kernel
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool valid) {
-    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    int sz = valid ? 16 : 0;
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int sz = valid ? 16 : 0;
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
 }
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.wait_all;\n" ::);
-}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
 // row r, float4 column q -> swizzled float4 index (conflict-free 4x4 tile reads)
-__device__ __forceinline__ int swz(int r, int q, int rs4) { return r * rs4 + (q ^ ((r >> 2) & 7)); }
+// (T = tile edge: lanes reading the same q of rows T*b + i, b consecutive, hit distinct banks)
+template <int T>
+__device__ __forceinline__ int swz(int r, int q, int rs4) {
+    return r * rs4 + (q ^ ((r / T) & 7));
+}
 
 // upper-triangle tile index t (bJ-major) -> (bI, bJ), bI <= bJ
 __device__ __forceinline__ void tile_decode(int t, int &bI, int &bJ) {
@@ -114,16 +136,181 @@ struct PropSmem {
     float dv[MAXK];
     int32_t perm[MAXK];  // position -> slot
     int32_t pos[MAXK];   // slot -> position
-    uint32_t fyj[MAXK];  // Fisher-Yates partner for position i
     int16_t e_tgt[MAXK];  // emitted message j: target slot
     int16_t e_id[MAXK];   // emitted message j: id slot
     int nmsg;
-    int vertex;
     unsigned long long list_base;
     unsigned long long ref_pairs;
 };
 
-template <int MAXK, int THREADS, int TPT>
+// T*T exact accumulators of a TxT tile over float4 columns [q0, q1)
+template <int T>
+__device__ __forceinline__ void tile_accumulate(float (&acc)[T * T], const float4 *__restrict__ rows, int rA, int rB,
+                                                int q0, int q1, int rs4) {
+#pragma unroll 2
+    for (int q = q0; q < q1; ++q) {
+        float4 A[T], B[T];
+#pragma unroll
+        for (int i = 0; i < T; ++i) A[i] = rows[swz<T>(rA + i, q, rs4)];
+#pragma unroll
+        for (int j = 0; j < T; ++j) B[j] = rows[swz<T>(rB + j, q, rs4)];
+#pragma unroll
+        for (int i = 0; i < T; ++i)
+#pragma unroll
+            for (int j = 0; j < T; ++j) {
+                float s = acc[i * T + j];
+                s = exact_step(s, A[i].x, B[j].x);
+                s = exact_step(s, A[i].y, B[j].y);
+                s = exact_step(s, A[i].z, B[j].z);
+                s = exact_step(s, A[i].w, B[j].w);
+                acc[i * T + j] = s;
+            }
+    }
+}
+
+// redirect condition of the T*T pairs of tile (bI, bJ), as bits in permutation space
+template <int MAXK, int T>
+__device__ __forceinline__ unsigned tile_epilogue(PropSmem<MAXK> &sm, const float (&acc)[T * T], int bI, int bJ,
+                                                  int k) {
+    constexpr int W = PropSmem<MAXK>::W;
+    unsigned npairs = 0;
+#pragma unroll
+    for (int i = 0; i < T; ++i)
+#pragma unroll
+        for (int j = 0; j < T; ++j) {
+            const int s = bI * T + i, u = bJ * T + j;
+            if (s < u && u < k && sm.ids[s] != TOMB && sm.ids[u] != TOMB) {
+                ++npairs;
+                const float d1 = sm.dv[s], d2 = sm.dv[u];
+                const float hi = d1 >= d2 ? d1 : d2;
+                if (acc[i * T + j] < hi) {
+                    const int x1 = sm.pos[s], x2 = sm.pos[u];
+                    // anchor = the member visited first (smaller position)
+                    const int xa = x1 < x2 ? x1 : x2, xb = x1 < x2 ? x2 : x1;
+                    const float dva = x1 < x2 ? d1 : d2, dvb = x1 < x2 ? d2 : d1;
+                    const unsigned long long bit = 1ull << (xb & 63);
+                    atomicOr((unsigned long long *)&sm.cond[xa * W + (xb >> 6)], bit);
+                    if (!(dvb >= dva)) atomicOr((unsigned long long *)&sm.afar[xa * W + (xb >> 6)], bit);
+                }
+            }
+        }
+    return npairs;
+}
+
+__device__ __forceinline__ uint64_t bits_above(int x, int w) {  // bits of word w at positions > x
+    const int b = x - w * 64;
+    if (b < 0) return ~0ull;
+    if (b >= 63) return 0ull;
+    return ~0ull << (b + 1);
+}
+__device__ __forceinline__ uint64_t bits_below(int f, int w) {  // bits of word w at positions < f
+    const int b = f - w * 64;
+    if (b <= 0) return 0ull;
+    if (b >= 64) return ~0ull;
+    return (1ull << b) - 1ull;
+}
+
+// Anchor-serial decision (_numba_kernels.py:158-185) by warp 0, over the masks.
+template <int MAXK>
+__device__ __forceinline__ void decide(PropSmem<MAXK> &sm, int k) {
+    constexpr int W = PropSmem<MAXK>::W;
+    const int lane = lane_id();
+    uint64_t live[W];
+#pragma unroll
+    for (int i = 0; i < W; ++i) live[i] = sm.live[i];
+    int nm = 0;
+    unsigned long long refp = 0;
+    for (int x0 = 0; x0 < k - 1; x0 += 32) {
+        const int x = x0 + lane;
+        uint64_t c[W], a[W];
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            c[i] = x < k - 1 ? sm.cond[x * W + i] : 0ull;
+            a[i] = x < k - 1 ? sm.afar[x * W + i] : 0ull;
+        }
+        int cur = x0;
+        while (true) {
+            const bool mylive = x < k - 1 && ((live[x >> 6] >> (x & 63)) & 1ull);
+            bool hit = false;
+#pragma unroll
+            for (int i = 0; i < W; ++i) hit |= (c[i] & live[i]) != 0ull;
+            const unsigned act = __ballot_sync(FULL, x >= cur && mylive && hit);
+            const int xa = act ? x0 + __ffs(act) - 1 : x0 + 32;
+            // live anchors in [cur, xa) have no live redirect partner: they visit every
+            // live partner after them (reference-semantics pair count)
+            if (x >= cur && x < xa && mylive) {
+                unsigned long long cnt = 0;
+#pragma unroll
+                for (int i = 0; i < W; ++i) cnt += __popcll(live[i] & bits_above(x, i));
+                refp += cnt;
+            }
+            if (!act) break;
+            // the active anchor's lane resolves its row
+            const int src = xa - x0;
+            int f = k;
+            uint64_t em[W];
+            unsigned long long visited = 0;
+            if (lane == src) {
+#pragma unroll
+                for (int i = 0; i < W; ++i) {
+                    const uint64_t m = a[i] & live[i];
+                    if (m && f == k) f = i * 64 + __ffsll((long long)m) - 1;
+                }
+#pragma unroll
+                for (int i = 0; i < W; ++i) {
+                    em[i] = c[i] & live[i] & ~a[i] & bits_below(f, i);
+                    // partners visited: live, position in (xa, f] (or (xa, k) without a break)
+                    const uint64_t vis = live[i] & bits_above(xa, i) & (f < k ? bits_below(f + 1, i) : ~0ull);
+                    visited += __popcll(vis);
+                }
+                refp += visited;
+            }
+            f = __shfl_sync(FULL, f, src);
+#pragma unroll
+            for (int i = 0; i < W; ++i) em[i] = __shfl_sync(FULL, em[i], src);
+            // emission records, partner-far messages in position order, then anchor-far
+            const int sa = sm.perm[xa];
+            int base = nm;
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                const uint64_t m = em[i];
+                if (!m) continue;
+                const uint32_t lo_ = (uint32_t)m, hi_ = (uint32_t)(m >> 32);
+                if ((lo_ >> lane) & 1u) {
+                    const int j = base + __popc(lo_ & ((1u << lane) - 1u));
+                    sm.e_tgt[j] = (int16_t)sa;
+                    sm.e_id[j] = (int16_t)sm.perm[i * 64 + lane];
+                }
+                if ((hi_ >> lane) & 1u) {
+                    const int j = base + __popc(lo_) + __popc(hi_ & ((1u << lane) - 1u));
+                    sm.e_tgt[j] = (int16_t)sa;
+                    sm.e_id[j] = (int16_t)sm.perm[i * 64 + 32 + lane];
+                }
+                base += __popcll(m);
+                live[i] &= ~m;
+            }
+            if (f < k) {
+                if (lane == 0) {
+                    sm.e_tgt[base] = (int16_t)sm.perm[f];
+                    sm.e_id[base] = (int16_t)sa;
+                }
+                ++base;
+                live[xa >> 6] &= ~(1ull << (xa & 63));
+            }
+            nm = base;
+            cur = xa + 1;
+        }
+    }
+    refp = warp_sum(refp);
+    if (lane == 0) {
+        sm.nmsg = nm;
+        sm.ref_pairs = refp;
+#pragma unroll
+        for (int i = 0; i < W; ++i) sm.live[i] = live[i];
+    }
+}
+
+template <int MAXK, int THREADS, int TPT, int T>
 __global__ void __launch_bounds__(THREADS) propagate_kernel(PropArgs a, int bin) {
     using S = PropSmem<MAXK>;
     constexpr int W = S::W;
@@ -136,6 +323,7 @@ __global__ void __launch_bounds__(THREADS) propagate_kernel(PropArgs a, int bin)
     const int32_t *blist = a.w.bins + (int64_t)bin * a.w.n;
     const int nq_total = (a.dim + 3) >> 2;  // float4 per row (ld % 4 == 0, pad cols are 0)
     const int rs4 = nq_total >= DC4 ? DC4 : ((nq_total + 7) & ~7);
+    const int nchunks = (nq_total + DC4 - 1) / DC4;
     const int cap = a.cap;
     unsigned long long pairs_local = 0;
 
@@ -146,13 +334,11 @@ __global__ void __launch_bounds__(THREADS) propagate_kernel(PropArgs a, int bin)
         const int32_t *rid = a.read_ids + v * cap;
         const float *rdv = a.read_dists + v * cap;
 
-        // ---- 1. pool row, permutation partners, bitset reset ----
-        const uint64_t pre = vertex_prefix(a.seed, a.stream_id, (uint64_t)vg);
+        // ---- 1. pool row + permutation positions, bitset reset ----
         for (int s = tid; s < k; s += THREADS) {
             sm.ids[s] = rid[s];
             sm.dv[s] = rdv[s];
-            sm.perm[s] = s;
-            if (a.order_code == 0 && s > 0) sm.fyj[s] = (uint32_t)(mix64(pre ^ (uint64_t)s) % (uint64_t)(s + 1));
+            if (a.order_code == 0) sm.pos[s] = a.w.pos8[v * cap + s];
         }
         for (int i = tid; i < k * W; i += THREADS) {
             sm.cond[i] = 0ull;
@@ -160,8 +346,7 @@ __global__ void __launch_bounds__(THREADS) propagate_kernel(PropArgs a, int bin)
         }
         __syncthreads();
 
-        // ---- 2. gather the first row chunk (overlaps the serial permutation below) ----
-        const int nchunks = (nq_total + DC4 - 1) / DC4;
+        // ---- 2. gather the pool rows (first 128-dim chunk) ----
         auto load_chunk = [&](int c) {
             const int q0 = c * DC4;
             const int nq = min(DC4, nq_total - q0);
@@ -171,192 +356,123 @@ __global__ void __launch_bounds__(THREADS) propagate_kernel(PropArgs a, int bin)
                 const int q = e - r * nq;
                 const int32_t id = sm.ids[r];
                 const float *src = a.data + (int64_t)(id < 0 ? 0 : id) * a.ld + (int64_t)(q0 + q) * 4;
-                cp_async16(&rows[swz(r, q, rs4)], src, id >= 0);
+                cp_async16(&rows[swz<T>(r, q, rs4)], src, id >= 0);
             }
-            asm volatile("cp.async.commit_group;\n" ::);
+            cp_async_commit();
         };
         load_chunk(0);
 
-        if (a.order_code == 0) {
-            // hash-driven Fisher-Yates (_numba_kernels.py:70-74): serial, one thread
-            if (tid == 0) {
-                for (int i = k - 1; i > 0; --i) {
-                    int j = (int)sm.fyj[i];
-                    int t = sm.perm[i];
-                    sm.perm[i] = sm.perm[j];
-                    sm.perm[j] = t;
-                }
-            }
-        } else {
+        if (a.order_code != 0) {
             // ascending debug order (:75-87): stable rank by (dist, id)
             for (int s = tid; s < k; s += THREADS) {
-                float ds = sm.dv[s];
-                int32_t is = sm.ids[s];
+                const float ds = sm.dv[s];
+                const int32_t is = sm.ids[s];
                 int r = 0;
                 for (int t = 0; t < k; ++t) {
-                    float dt = sm.dv[t];
-                    int32_t it2 = sm.ids[t];
+                    const float dt = sm.dv[t];
+                    const int32_t it2 = sm.ids[t];
                     r += (dt < ds || (dt == ds && (it2 < is || (it2 == is && t < s)))) ? 1 : 0;
                 }
                 sm.pos[s] = r;
             }
             __syncthreads();
-            for (int s = tid; s < k; s += THREADS) sm.perm[sm.pos[s]] = s;
         }
+        for (int s = tid; s < k; s += THREADS) sm.perm[sm.pos[s]] = s;
         __syncthreads();
-        for (int x = tid; x < k; x += THREADS) sm.pos[sm.perm[x]] = x;
-        if (tid < W) {
-            uint64_t m = 0;
-            for (int b = 0; b < 64; ++b) {
-                int x = tid * 64 + b;
-                if (x < k && sm.ids[sm.perm[x]] != TOMB) m |= 1ull << b;
+        if (tid < 32) {
+            // live mask by permutation position (one ballot per 32 positions)
+            for (int x0 = 0; x0 < W * 64; x0 += 32) {
+                const int x = x0 + tid;
+                const bool lv = x < k && sm.ids[sm.perm[x]] != TOMB;
+                const unsigned b = __ballot_sync(FULL, lv);
+                if (tid == 0) {
+                    if ((x0 & 63) == 0) sm.live[x0 >> 6] = (uint64_t)b;
+                    else sm.live[x0 >> 6] |= (uint64_t)b << 32;
+                }
             }
-            sm.live[tid] = m;
         }
 
-        // ---- 3. all-pairs exact distances, 4x4 register tiles, upper triangle ----
-        const int nb = (k + 3) >> 2;
+        // ---- 3. all-pairs exact distances, TxT register tiles, upper triangle ----
+        const int nb = (k + T - 1) / T;
         const int ntiles = nb * (nb + 1) / 2;
-        for (int g0 = 0; g0 < ntiles; g0 += THREADS * TPT) {
-            float acc[TPT][16];
+        if (nchunks == 1) {
+            cp_async_wait_all();
+            __syncthreads();
+            for (int t = tid; t < ntiles; t += THREADS) {
+                int bI, bJ;
+                tile_decode(t, bI, bJ);
+                float acc[T * T];
 #pragma unroll
-            for (int tt = 0; tt < TPT; ++tt)
+                for (int p = 0; p < T * T; ++p) acc[p] = 0.0f;
+                tile_accumulate<T>(acc, rows, bI * T, bJ * T, 0, nq_total, rs4);
+                pairs_local += tile_epilogue<MAXK, T>(sm, acc, bI, bJ, k);
+            }
+        } else {
+            for (int g0 = 0; g0 < ntiles; g0 += THREADS * TPT) {
+                float acc[TPT][T * T];
 #pragma unroll
-                for (int p = 0; p < 16; ++p) acc[tt][p] = 0.0f;
-            for (int c = 0; c < nchunks; ++c) {
-                if (nchunks > 1 && (c > 0 || g0 > 0)) {
-                    __syncthreads();  // everyone done with the previous chunk
-                    load_chunk(c);
+                for (int tt = 0; tt < TPT; ++tt)
+#pragma unroll
+                    for (int p = 0; p < T * T; ++p) acc[tt][p] = 0.0f;
+                for (int c = 0; c < nchunks; ++c) {
+                    if (c > 0 || g0 > 0) {
+                        __syncthreads();  // everyone done with the previous chunk
+                        load_chunk(c);
+                    }
+                    cp_async_wait_all();
+                    __syncthreads();
+                    const int nq = min(DC4, nq_total - c * DC4);
+#pragma unroll
+                    for (int tt = 0; tt < TPT; ++tt) {
+                        const int t = g0 + tt * THREADS + tid;
+                        if (t < ntiles) {
+                            int bI, bJ;
+                            tile_decode(t, bI, bJ);
+                            tile_accumulate<T>(acc[tt], rows, bI * T, bJ * T, 0, nq, rs4);
+                        }
+                    }
                 }
-                cp_async_wait_all();
-                __syncthreads();
-                const int nq = min(DC4, nq_total - c * DC4);
 #pragma unroll
                 for (int tt = 0; tt < TPT; ++tt) {
                     const int t = g0 + tt * THREADS + tid;
                     if (t < ntiles) {
                         int bI, bJ;
                         tile_decode(t, bI, bJ);
-                        const int rA = bI * 4, rB = bJ * 4;
-#pragma unroll 2
-                        for (int q = 0; q < nq; ++q) {
-                            float4 A[4], B[4];
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) A[i] = rows[swz(rA + i, q, rs4)];
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) B[j] = rows[swz(rB + j, q, rs4)];
-#pragma unroll
-                            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                                for (int j = 0; j < 4; ++j) {
-                                    float s = acc[tt][i * 4 + j];
-                                    s = exact_step(s, A[i].x, B[j].x);
-                                    s = exact_step(s, A[i].y, B[j].y);
-                                    s = exact_step(s, A[i].z, B[j].z);
-                                    s = exact_step(s, A[i].w, B[j].w);
-                                    acc[tt][i * 4 + j] = s;
-                                }
-                        }
+                        pairs_local += tile_epilogue<MAXK, T>(sm, acc[tt], bI, bJ, k);
                     }
-                }
-            }
-            // epilogue: redirect condition per pair, as bits in permutation-position space
-#pragma unroll
-            for (int tt = 0; tt < TPT; ++tt) {
-                const int t = g0 + tt * THREADS + tid;
-                if (t < ntiles) {
-                    int bI, bJ;
-                    tile_decode(t, bI, bJ);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const int s = bI * 4 + i, u = bJ * 4 + j;
-                            if (s < u && u < k && sm.ids[s] != TOMB && sm.ids[u] != TOMB) {
-                                ++pairs_local;
-                                const float d1 = sm.dv[s], d2 = sm.dv[u];
-                                const float hi = d1 >= d2 ? d1 : d2;
-                                if (acc[tt][i * 4 + j] < hi) {
-                                    const int x1 = sm.pos[s], x2 = sm.pos[u];
-                                    // anchor = the member visited first (smaller position)
-                                    const int xa = x1 < x2 ? x1 : x2, xb = x1 < x2 ? x2 : x1;
-                                    const float dva = x1 < x2 ? d1 : d2, dvb = x1 < x2 ? d2 : d1;
-                                    const uint64_t bit = 1ull << (xb & 63);
-                                    atomicOr((unsigned long long *)&sm.cond[xa * W + (xb >> 6)], bit);
-                                    if (!(dvb >= dva)) atomicOr((unsigned long long *)&sm.afar[xa * W + (xb >> 6)], bit);
-                                }
-                            }
-                        }
                 }
             }
         }
         __syncthreads();
 
-        // ---- 4. anchor-serial decision over the masks (one thread) ----
-        if (tid == 0) {
-            uint64_t live[W];
-#pragma unroll
-            for (int i = 0; i < W; ++i) live[i] = sm.live[i];
-            int nm = 0;
-            unsigned long long refp = 0;
-            for (int x = 0; x < k - 1; ++x) {
-                if (!((live[x >> 6] >> (x & 63)) & 1ull)) continue;
-                // first partner that makes the anchor the farther one
-                int f = k;
-#pragma unroll
-                for (int i = 0; i < W; ++i) {
-                    uint64_t m = sm.afar[x * W + i] & live[i];
-                    if (m && f == k) f = i * 64 + __ffsll((long long)m) - 1;
-                }
-                // visited partners: live, position in (x, f]  (reference-semantics pair count)
-#pragma unroll
-                for (int i = 0; i < W; ++i) {
-                    uint64_t m = live[i];
-                    int lo_b = x + 1 - i * 64, hi_b = (f < k ? f : k - 1) - i * 64;
-                    if (hi_b < 0 || lo_b > 63) continue;
-                    if (lo_b > 0) m &= ~0ull << lo_b;
-                    if (hi_b < 63) m &= (2ull << hi_b) - 1ull;
-                    refp += __popcll(m);
-                }
-                const int sa = sm.perm[x];
-#pragma unroll
-                for (int i = 0; i < W; ++i) {
-                    uint64_t m = sm.cond[x * W + i] & live[i];
-                    int hb = f - i * 64;  // keep bits < f
-                    if (hb <= 0) m = 0;
-                    else if (hb < 64) m &= (1ull << hb) - 1ull;
-                    uint64_t em = m & ~sm.afar[x * W + i];
-                    while (em) {
-                        int b = __ffsll((long long)em) - 1;
-                        em &= em - 1;
-                        int y = i * 64 + b;
-                        sm.e_tgt[nm] = (int16_t)sa;
-                        sm.e_id[nm] = (int16_t)sm.perm[y];
-                        ++nm;
-                        live[i] &= ~(1ull << b);
-                    }
-                }
-                if (f < k) {
-                    sm.e_tgt[nm] = (int16_t)sm.perm[f];
-                    sm.e_id[nm] = (int16_t)sa;
-                    ++nm;
-                    live[x >> 6] &= ~(1ull << (x & 63));
-                }
-            }
-            sm.nmsg = nm;
-            sm.ref_pairs = refp;
-#pragma unroll
-            for (int i = 0; i < W; ++i) sm.live[i] = live[i];
-            if (!a.slice_mode && nm > 0) sm.list_base = atomicAdd(&a.w.ctr[C_LIST], (unsigned long long)nm);
+        // ---- 4. anchor-serial decision over the masks (warp 0) ----
+        if (tid < 32) {
+            decide<MAXK>(sm, k);
+            if (tid == 0 && !a.slice_mode && sm.nmsg > 0)
+                sm.list_base = atomicAdd(&a.w.ctr[C_LIST], (unsigned long long)sm.nmsg);
         }
         __syncthreads();
 
-        // ---- 5. emit redirects (exact distance re-evaluated from L2-resident rows) ----
+        // ---- 5. emit redirects: exact distance re-evaluated from the staged rows ----
         const int nm = sm.nmsg;
         for (int j = tid; j < nm; j += THREADS) {
-            const int32_t tgt = sm.ids[sm.e_tgt[j]];
-            const int32_t id = sm.ids[sm.e_id[j]];
-            const float d = exact_sqdist_global(a.data + (int64_t)tgt * a.ld, a.data + (int64_t)id * a.ld, a.dim);
+            const int st = sm.e_tgt[j], si = sm.e_id[j];
+            const int32_t tgt = sm.ids[st];
+            const int32_t id = sm.ids[si];
+            float d;
+            if (nchunks == 1) {
+                d = 0.0f;
+                for (int q = 0; q < nq_total; ++q) {
+                    const float4 x = rows[swz<T>(st, q, rs4)];
+                    const float4 y = rows[swz<T>(si, q, rs4)];
+                    d = exact_step(d, x.x, y.x);
+                    d = exact_step(d, x.y, y.y);
+                    d = exact_step(d, x.z, y.z);
+                    d = exact_step(d, x.w, y.w);
+                }
+            } else {
+                d = exact_sqdist_global(a.data + (int64_t)tgt * a.ld, a.data + (int64_t)id * a.ld, a.dim);
+            }
             if (a.slice_mode) {
                 a.msg_tgt[v * cap + j] = tgt;
                 a.msg_id[v * cap + j] = id;
@@ -379,28 +495,26 @@ __global__ void __launch_bounds__(THREADS) propagate_kernel(PropArgs a, int bin)
             const bool alive = (sm.live[x >> 6] >> (x & 63)) & 1ull;
             if (!alive && sm.ids[s] != TOMB) a.read_ids[v * cap + s] = TOMB;
         }
-        if (a.slice_mode) {
+        if (a.slice_mode && tid < 32) {
             // survivors in slot order after the redirects (:186-191)
-            if (tid < 32) {
-                int base = nm;
-                for (int s0 = 0; s0 < k; s0 += 32) {
-                    const int s = s0 + tid;
-                    bool alive = false;
-                    if (s < k) {
-                        const int x = sm.pos[s];
-                        alive = ((sm.live[x >> 6] >> (x & 63)) & 1ull) && sm.ids[s] != TOMB;
-                    }
-                    const unsigned bal = __ballot_sync(FULL, alive);
-                    if (alive) {
-                        const int o = base + __popc(bal & ((1u << tid) - 1));
-                        a.msg_tgt[v * cap + o] = (int32_t)vg;
-                        a.msg_id[v * cap + o] = sm.ids[s];
-                        a.msg_dist[v * cap + o] = sm.dv[s];
-                    }
-                    base += __popc(bal);
+            int base = nm;
+            for (int s0 = 0; s0 < k; s0 += 32) {
+                const int s = s0 + tid;
+                bool alive = false;
+                if (s < k) {
+                    const int x = sm.pos[s];
+                    alive = ((sm.live[x >> 6] >> (x & 63)) & 1ull) && sm.ids[s] != TOMB;
                 }
-                if (tid == 0) a.msg_cnt[v] = base;
+                const unsigned bal = __ballot_sync(FULL, alive);
+                if (alive) {
+                    const int o = base + __popc(bal & ((1u << tid) - 1));
+                    a.msg_tgt[v * cap + o] = (int32_t)vg;
+                    a.msg_id[v * cap + o] = sm.ids[s];
+                    a.msg_dist[v * cap + o] = sm.dv[s];
+                }
+                base += __popc(bal);
             }
+            if (tid == 0) a.msg_cnt[v] = base;
         }
         if (tid == 0 && a.stats) {
             if (nm) atomicAdd((unsigned long long *)&a.stats[GRNND_ST_REDIRECTS], (unsigned long long)nm);
@@ -417,10 +531,11 @@ __global__ void __launch_bounds__(THREADS) propagate_kernel(PropArgs a, int bin)
 // ---------------------------------------------------------------------------------
 // host launcher
 // ---------------------------------------------------------------------------------
-template <int MAXK, int THREADS, int TPT>
+template <int MAXK, int THREADS, int TPT, int T>
 static int launch_bin(const PropArgs &a, int bin, int num_sms, cudaStream_t st) {
-    auto kern = propagate_kernel<MAXK, THREADS, TPT>;
-    const int kmax = MAXK < a.cap ? MAXK : a.cap;
+    auto kern = propagate_kernel<MAXK, THREADS, TPT, T>;
+    // TxT tiles read rows up to round_up(k, T) - 1: size the slab for that
+    const int kmax = ((MAXK < a.cap ? MAXK : a.cap) + T - 1) / T * T;
     const int nq_total = (a.dim + 3) >> 2;
     const int rs4 = nq_total >= DC4 ? DC4 : ((nq_total + 7) & ~7);
     const size_t smem = align_up(sizeof(PropSmem<MAXK>), 128) + (size_t)kmax * rs4 * 16;
@@ -445,19 +560,19 @@ int launch_propagate(const PropArgs &a, cudaStream_t st) {
     GRNND_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
     const int64_t n = a.hi - a.lo;
     if (n <= 0) return GRNND_OK;
-    // counters: bins
     GRNND_CUDA(cudaMemsetAsync(a.w.ctr + C_BIN0, 0, sizeof(unsigned long long) * NBINS, st));
-    const int tb = 256;
-    bin_kernel<<<(unsigned)((n + tb - 1) / tb), tb, 0, st>>>(
-        a.read_count, n, a.cap, a.w, a.stats, a.slice_mode, a.read_ids, a.read_dists, a.lo,
-        a.msg_tgt, a.msg_id, a.msg_dist, a.msg_cnt);
+    const int tb = 128;
+    bin_kernel<<<(unsigned)((n + tb - 1) / tb), tb, 0, st>>>(a.read_count, n, a.cap, a.w, a.stats, a.slice_mode,
+                                                            a.read_ids, a.read_dists, a.lo, a.seed, a.stream_id,
+                                                            a.order_code, a.msg_tgt, a.msg_id, a.msg_dist,
+                                                            a.msg_cnt);
     GRNND_TRY(check_launch("bin_kernel"));
     // largest k first so long CTAs start early
-    if (a.cap > 128) GRNND_TRY((launch_bin<256, 256, 3>(a, 5, num_sms, st)));
-    if (a.cap > 64) GRNND_TRY((launch_bin<128, 256, 3>(a, 4, num_sms, st)));
-    if (a.cap > 32) GRNND_TRY((launch_bin<64, 128, 2>(a, 3, num_sms, st)));
-    if (a.cap > 16) GRNND_TRY((launch_bin<32, 64, 1>(a, 2, num_sms, st)));
-    if (a.cap > 1) GRNND_TRY((launch_bin<16, 32, 1>(a, 1, num_sms, st)));
+    if (a.cap > 128) GRNND_TRY((launch_bin<256, 256, 3, 4>(a, 5, num_sms, st)));
+    if (a.cap > 64) GRNND_TRY((launch_bin<128, 128, 3, 4>(a, 4, num_sms, st)));
+    if (a.cap > 32) GRNND_TRY((launch_bin<64, 64, 3, 4>(a, 3, num_sms, st)));
+    if (a.cap > 16) GRNND_TRY((launch_bin<32, 64, 3, 2>(a, 2, num_sms, st)));
+    if (a.cap > 1) GRNND_TRY((launch_bin<16, 32, 2, 2>(a, 1, num_sms, st)));
     return GRNND_OK;
 }
 

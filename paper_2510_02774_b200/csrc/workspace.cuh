@@ -39,6 +39,8 @@ struct Workspace {
     int64_t *scan_tmp;   // [scan blocks + 1]
     int32_t *bins;       // [n] vertex lists, bin b at bins + bin_off[b] ... (packed by counts)
     int32_t *heavy;      // [n] heavy segment ids
+    uint8_t *pos8;       // [n, cap] permutation position of each pool slot (this round)
+    int32_t cap;
     int64_t n;
     int64_t msg_capacity;
 };
@@ -50,7 +52,7 @@ constexpr int SCAN_ITEMS = 2048;  // elements per scan block
 inline int64_t scan_blocks(int64_t n) { return (n + SCAN_ITEMS - 1) / SCAN_ITEMS; }
 
 // Layout: computes offsets; with base == nullptr returns the byte size only.
-inline size_t carve(Workspace *w, void *base, int64_t n, int64_t msg_capacity) {
+inline size_t carve(Workspace *w, void *base, int64_t n, int32_t cap, int64_t msg_capacity) {
     size_t off = 0;
     auto take = [&](size_t bytes) -> void * {
         off = align_up(off, 256);
@@ -78,6 +80,8 @@ inline size_t carve(Workspace *w, void *base, int64_t n, int64_t msg_capacity) {
     t.scan_tmp = (int64_t *)take(8 * (size_t)(scan_blocks((int64_t)N) + 2 + 128));
     t.bins = (int32_t *)take(4 * N * NBINS);
     t.heavy = (int32_t *)take(4 * N);
+    t.pos8 = (uint8_t *)take(N * (size_t)(cap > 0 ? cap : 1));
+    t.cap = cap;
     t.n = n;
     t.msg_capacity = msg_capacity;
     if (w) *w = t;

@@ -14,7 +14,7 @@ ROOT = Path(__file__).resolve().parents[1]
 
 def header_functions():
     text = (ROOT / "include" / "grnnd_b200.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char \*)\s*(grnnd_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char \*|unsigned long long)\s*(grnnd_\w+)\s*\(", text, re.M)))
 
 
 def test_library_exports_every_declared_symbol():
