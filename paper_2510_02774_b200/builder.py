@@ -241,6 +241,22 @@ class _DevicePools:
         _lib.call("grnnd_reverse_round", C.byref(p), float(rho), _stream(self.dev))
         self.swap()
 
+    def update_split(self, seed: int, stream_id: int, order_code: int, stats: torch.Tensor,
+                     ev: tuple | None = None) -> None:
+        """update() as its two halves with optional CUDA events (before emit, after emit,
+        after apply) for per-phase timing on the launching stream."""
+        p = self.struct(stats)
+        st = _stream(self.dev)
+        if ev:
+            ev[0].record()
+        _lib.call("grnnd_update_emit", C.byref(p), seed & MASK64, stream_id & MASK64, order_code, st)
+        if ev:
+            ev[1].record()
+        _lib.call("grnnd_apply_emitted", C.byref(p), 0, st)
+        if ev:
+            ev[2].record()
+        self.swap()
+
     def finalize(self, offsets: torch.Tensor, nbrs: torch.Tensor, bad: torch.Tensor) -> None:
         _lib.call(
             "grnnd_finalize", self.read_ids.data_ptr(), self.read_dists.data_ptr(), self.read_count.data_ptr(),
@@ -472,6 +488,52 @@ def build(dataset: Dataset, params: BuildParams, pair_order: PairOrder = "disord
         if report_stats is not None:
             report_stats.append(s)
     return graph
+
+
+class DeviceBuild:
+    """A reusable build engine over device-resident vectors (the bench's timed step and
+    the building block of the sharded multi-GPU build).  ``run()`` = init + all rounds +
+    finalize, entirely asynchronous; results stay in HBM."""
+
+    def __init__(self, data_dev: torch.Tensor, dim: int, params: BuildParams,
+                 pair_order: PairOrder = "disordered"):
+        self.params = effective_params(params, int(data_dev.shape[0]))
+        validate_params(self.params, int(data_dev.shape[0]))
+        self.order = _ORDER_CODES[pair_order]
+        self.pools = _DevicePools(data_dev, dim, self.params.R)
+        self.rounds = num_rounds(self.params)
+        self.stats = torch.zeros((self.rounds, _lib.NSTATS), dtype=torch.int64, device=self.pools.dev)
+        self.kinds: list[str] = []
+
+    def run(self, phase_events: list | None = None):
+        """One full build.  phase_events, if given, receives one (start, emitted, applied)
+        CUDA-event triple per update round."""
+        p, pools = self.params, self.pools
+        self.stats.zero_()
+        self.kinds = []
+        fail = pools.init(p.S, p.seed)
+        i = 0
+        round_index = 0
+        for t1 in range(1, p.T1 + 1):
+            for _ in range(p.T2):
+                ev = None
+                if phase_events is not None:
+                    ev = tuple(torch.cuda.Event(enable_timing=True) for _ in range(3))
+                    phase_events.append(ev)
+                pools.update_split(p.seed, STREAM_ROUND_BASE + round_index, self.order, self.stats[i], ev)
+                round_index += 1
+                self.kinds.append("update")
+                i += 1
+            if t1 != p.T1:
+                pools.reverse(p.rho, self.stats[i])
+                self.kinds.append("reverse")
+                i += 1
+        offsets, nbrs, bad = _finalize_device(pools)
+        return offsets, nbrs, bad, fail
+
+    def round_stats(self) -> list[RoundStats]:
+        rows = self.stats.cpu().numpy()
+        return [RoundStats.from_counters(k, c) for k, c in zip(self.kinds, rows)]
 
 
 def build_fixed_degree(dataset: Dataset, params: BuildParams, pair_order: PairOrder = "disordered",

@@ -310,7 +310,9 @@ __device__ __forceinline__ void decide(PropSmem<MAXK> &sm, int k) {
     }
 }
 
-template <int MAXK, int THREADS, int TPT, int T>
+// MULTI: D > 128, rows staged 128 dims at a time with accumulators held across chunks
+// (a separate instantiation keeps the common D <= 128 kernel's register count low)
+template <int MAXK, int THREADS, int TPT, int T, bool MULTI>
 __global__ void __launch_bounds__(THREADS) propagate_kernel(PropArgs a, int bin) {
     using S = PropSmem<MAXK>;
     constexpr int W = S::W;
@@ -395,7 +397,7 @@ __global__ void __launch_bounds__(THREADS) propagate_kernel(PropArgs a, int bin)
         // ---- 3. all-pairs exact distances, TxT register tiles, upper triangle ----
         const int nb = (k + T - 1) / T;
         const int ntiles = nb * (nb + 1) / 2;
-        if (nchunks == 1) {
+        if (!MULTI) {
             cp_async_wait_all();
             __syncthreads();
             for (int t = tid; t < ntiles; t += THREADS) {
@@ -460,7 +462,7 @@ __global__ void __launch_bounds__(THREADS) propagate_kernel(PropArgs a, int bin)
             const int32_t tgt = sm.ids[st];
             const int32_t id = sm.ids[si];
             float d;
-            if (nchunks == 1) {
+            if (!MULTI) {
                 d = 0.0f;
                 for (int q = 0; q < nq_total; ++q) {
                     const float4 x = rows[swz<T>(st, q, rs4)];
@@ -531,9 +533,9 @@ __global__ void __launch_bounds__(THREADS) propagate_kernel(PropArgs a, int bin)
 // ---------------------------------------------------------------------------------
 // host launcher
 // ---------------------------------------------------------------------------------
-template <int MAXK, int THREADS, int TPT, int T>
-static int launch_bin(const PropArgs &a, int bin, int num_sms, cudaStream_t st) {
-    auto kern = propagate_kernel<MAXK, THREADS, TPT, T>;
+template <int MAXK, int THREADS, int TPT, int T, bool MULTI>
+static int launch_bin_impl(const PropArgs &a, int bin, int num_sms, cudaStream_t st) {
+    auto kern = propagate_kernel<MAXK, THREADS, TPT, T, MULTI>;
     // TxT tiles read rows up to round_up(k, T) - 1: size the slab for that
     const int kmax = ((MAXK < a.cap ? MAXK : a.cap) + T - 1) / T * T;
     const int nq_total = (a.dim + 3) >> 2;
@@ -552,6 +554,12 @@ static int launch_bin(const PropArgs &a, int bin, int num_sms, cudaStream_t st) 
     }
     kern<<<num_sms * per_sm, THREADS, smem, st>>>(a, bin);
     return check_launch("propagate_kernel");
+}
+
+template <int MAXK, int THREADS, int TPT, int T>
+static int launch_bin(const PropArgs &a, int bin, int num_sms, cudaStream_t st) {
+    if (a.dim <= DC4 * 4) return launch_bin_impl<MAXK, THREADS, TPT, T, false>(a, bin, num_sms, st);
+    return launch_bin_impl<MAXK, THREADS, TPT, T, true>(a, bin, num_sms, st);
 }
 
 int launch_propagate(const PropArgs &a, cudaStream_t st) {
