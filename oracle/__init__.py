@@ -64,6 +64,13 @@ def lib():
             None,
             [_f32p, _i64, _i32, _i32p, _f32p, _i32p, _i32, _u64, _u64, _i32, _i32p, _i32p, _f32p, _i32p],
         ),
+        "orc_gen_update_messages_lo": (
+            None,
+            [_f32p, _i64, _i64, _i32, _i32p, _f32p, _i32p, _i32, _u64, _u64, _i32, _i32p, _i32p, _f32p, _i32p],
+        ),
+        "orc_gen_reverse_messages_lo": (
+            None, [_i32p, _f32p, _i32p, _i64, _i64, _i32, C.c_double, _i32p, _i32p, _f32p, _i32p]
+        ),
         "orc_reverse_count": (_i32, [C.c_double, _i32]),
         "orc_gen_reverse_messages": (
             None, [_i32p, _f32p, _i32p, _i64, _i32, C.c_double, _i32p, _i32p, _f32p, _i32p]
@@ -173,6 +180,33 @@ def gen_update_messages(data, read_ids, read_dists, read_count, seed, stream, or
     lib().orc_gen_update_messages(
         data, n, data.shape[1], read_ids, _f32(read_dists), _i32a(read_count), cap,
         seed & M64, stream & M64, order_code, mt, mi, md, mc,
+    )
+    return mt, mi, md, mc
+
+
+def gen_update_messages_lo(data, lo, read_ids, read_dists, read_count, seed, stream, order_code):
+    """gen_update_messages on owned rows [lo, lo + n): returns slices; mutates read_ids."""
+    data = _f32(data)
+    n, cap = read_ids.shape
+    mt = np.full(n * cap, -1, np.int32)
+    mi = np.full(n * cap, -1, np.int32)
+    md = np.zeros(n * cap, np.float32)
+    mc = np.zeros(n, np.int32)
+    lib().orc_gen_update_messages_lo(
+        data, lo, n, data.shape[1], read_ids, _f32(read_dists), _i32a(read_count), cap,
+        seed & M64, stream & M64, order_code, mt, mi, md, mc,
+    )
+    return mt, mi, md, mc
+
+
+def gen_reverse_messages_lo(lo, read_ids, read_dists, read_count, rho):
+    n, cap = read_ids.shape
+    mt = np.full(n * cap, -1, np.int32)
+    mi = np.full(n * cap, -1, np.int32)
+    md = np.zeros(n * cap, np.float32)
+    mc = np.zeros(n, np.int32)
+    lib().orc_gen_reverse_messages_lo(
+        _i32a(read_ids), _f32(read_dists), _i32a(read_count), lo, n, cap, float(rho), mt, mi, md, mc
     )
     return mt, mi, md, mc
 

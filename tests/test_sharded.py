@@ -1,0 +1,152 @@
+"""Multi-GPU path.
+
+* CPU (gloo, world_size 2): the sharded round structure -- owned ID ranges, rank
+  bucketing, exchange_all_to_all (the same host function the NCCL path uses), keyed
+  regrouping with the own-entry splice -- driven with oracle compute, must reproduce the
+  single-process reference build bit for bit.
+* GPU: build_virtual_shards (P ranks' kernels on one GPU, exchange by concatenation)
+  must equal build() and the oracle bit for bit.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2510_02774_b200.core import generate
+from paper_2510_02774_b200.sharded import FIELDS, exchange_all_to_all, shard_bounds
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _apply_ordered(rows, R, lo, kind, incoming, own_ids, own_d, own_cnt):
+    """Per owned target: incoming sorted by key, own entries spliced at src == tgt
+    (update) or after everything (reverse); three-stage insert via the oracle."""
+    key, tgt, mid, md = incoming
+    flat_id, flat_d, starts = [], [], [0]
+    for r in range(rows):
+        t = lo + r
+        sel = np.flatnonzero(tgt == t)
+        sel = sel[np.argsort(key[sel], kind="stable")]
+        split = np.searchsorted(key[sel], t * R) if kind == 0 else len(sel)
+        own = [(own_ids[r, s], own_d[r, s]) for s in range(own_cnt[r]) if own_ids[r, s] != -1]
+        seq = [(mid[i], md[i]) for i in sel[:split]] + own + [(mid[i], md[i]) for i in sel[split:]]
+        flat_id += [x for x, _ in seq]
+        flat_d += [d for _, d in seq]
+        starts.append(len(flat_id))
+    wi = np.full((rows, R), -1, np.int32)
+    wd = np.full((rows, R), np.inf, np.float32)
+    wc = np.zeros(rows, np.int32)
+    n = len(flat_id)
+    oracle.apply_grouped_messages(wi, wd, wc, np.array(flat_id, np.int32), np.array(flat_d, np.float32),
+                                  np.arange(n, dtype=np.int64), np.array(starts, np.int64))
+    return wi, wd, wc
+
+
+def _worker(rank, world, port, cfg, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, dim, S, R, T1, T2, rho, seed = cfg
+        data = generate(n, dim, "gaussian", seed=seed).data
+        b = shard_bounds(n, world)
+        lo, hi = b[rank], b[rank + 1]
+        rows = hi - lo
+        ids_all, _ = oracle.sample_initial(n, S, seed)
+        d_all = oracle.init_dists(data, ids_all)
+        rid = np.full((rows, R), -1, np.int32)
+        rd = np.full((rows, R), np.inf, np.float32)
+        rc = np.full(rows, S, np.int32)
+        rid[:, :S] = ids_all[lo:hi]
+        rd[:, :S] = d_all[lo:hi]
+        ri = 0
+        for t1 in range(1, T1 + 1):
+            for kind in [0] * T2 + ([1] if t1 != T1 else []):
+                if kind == 0:
+                    mt, mi, md, mc = oracle.gen_update_messages_lo(data, lo, rid, rd, rc, seed, 1 + ri, 0)
+                    ri += 1
+                else:
+                    mt, mi, md, mc = oracle.gen_reverse_messages_lo(lo, rid, rd, rc, rho)
+                # outgoing = redirects / reverse edges; survivors stay home (not sent)
+                msgs = []
+                for v in range(rows):
+                    for j in range(mc[v]):
+                        t = mt[v * R + j]
+                        if kind == 1 or t != lo + v:
+                            msgs.append(((lo + v) * R + j, t, mi[v * R + j], md[v * R + j]))
+                owner = np.searchsorted(np.array(b[1:]), [m[1] for m in msgs], side="right") if msgs else []
+                order = np.argsort(owner, kind="stable") if msgs else []
+                msgs = [msgs[i] for i in order]
+                send_counts = [int(np.sum(np.asarray(owner) == r)) for r in range(world)]
+                cap = max(sum(send_counts), 1)
+                out = {"key": torch.tensor([m[0] for m in msgs] + [0] * (cap - len(msgs)), dtype=torch.int64),
+                       "tgt": torch.tensor([m[1] for m in msgs] + [0] * (cap - len(msgs)), dtype=torch.int32),
+                       "id": torch.tensor([m[2] for m in msgs] + [0] * (cap - len(msgs)), dtype=torch.int32),
+                       "dist": torch.tensor([m[3] for m in msgs] + [0] * (cap - len(msgs)), dtype=torch.float32)}
+                inb = {f: torch.zeros(n * R, dtype=dt) for f, dt in FIELDS}
+                n_in = exchange_all_to_all(out, send_counts, inb)
+                incoming = tuple(inb[f][:n_in].numpy() for f, _ in FIELDS)
+                rid, rd, rc = _apply_ordered(rows, R, lo, kind, incoming, rid, rd, rc)
+        off, nb = oracle.finalize(rid, rd, rc)
+        parts = [None] * world
+        dist.all_gather_object(parts, (off, nb))
+        if rank == 0:
+            out_q.put(parts)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_sharded_exchange_cpu_gloo_bit_exact(world):
+    cfg = (600, 8, 8, 16, 2, 3, 0.6, 3)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    base, offs, nbrs = 0, [], []
+    for off, nb in parts:
+        offs.append(off[:-1] + base)
+        nbrs.append(nb)
+        base += int(off[-1])
+    offsets = np.concatenate(offs + [np.array([base])])
+    n, dim, S, R, T1, T2, rho, seed = cfg
+    want_off, want_nb = oracle.build(generate(n, dim, "gaussian", seed=seed).data, S, R, T1, T2, rho, seed)
+    assert np.array_equal(offsets, want_off)
+    assert np.array_equal(np.concatenate(nbrs), want_nb)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_virtual_shards_bit_exact(world):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2510_02774_b200 as g
+    from paper_2510_02774_b200.sharded import build_virtual_shards
+
+    ds = generate(5000, 32, "gaussian", seed=4)
+    params = g.BuildParams(S=12, R=32, T1=3, T2=3, rho=0.6, seed=4)
+    log1, logp = [], []
+    one = g.build(ds, params, report_stats=log1)
+    shard = build_virtual_shards(ds, params, world, report_stats=logp)
+    assert np.array_equal(shard.offsets, one.offsets)
+    assert np.array_equal(shard.neighbor_ids, one.neighbor_ids)
+    assert [s.inserted for s in logp] == [s.inserted for s in log1]
+    off, nb = oracle.build(ds.data, 12, 32, 3, 3, 0.6, 4)
+    assert np.array_equal(shard.neighbor_ids, nb)
