@@ -199,6 +199,11 @@ int grnnd_finalize(const int32_t *ids, const float *dists, const int32_t *counts
                    int32_t cap, int64_t *offsets, int32_t *nbrs, int64_t *bad_flag,
                    void *workspace, size_t workspace_bytes, grnnd_stream_t s);
 
+/* grnnd_finalize on the read side of a (possibly sharded) pool set: rows lo..hi-1, ids
+ * validated against [0, n_total) and the global owner id. */
+int grnnd_finalize_pools(const grnnd_pools *p, int64_t *offsets, int32_t *nbrs, int64_t *bad_flag,
+                         grnnd_stream_t s);
+
 /* Dataset.validate finiteness scan (core.py:70-71) on device: *bad_flag = 1 if any of the
  * first dim columns of data[n, ld] is NaN/inf. */
 int grnnd_check_finite(const float *data, int64_t n, int32_t dim, int32_t ld, int64_t *bad_flag,

@@ -86,6 +86,7 @@ _SIGS = {
     "grnnd_round_apply": (C.c_int, [C.POINTER(Pools), _i32, _i64, _vp]),
     "grnnd_finalize": (C.c_int, [_vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "grnnd_sorted_rows": (C.c_int, [_vp, _vp, _vp, _i64, _i32, _vp, _vp]),
+    "grnnd_finalize_pools": (C.c_int, [C.POINTER(Pools), _vp, _vp, _vp, _vp]),
     "grnnd_check_finite": (C.c_int, [_vp, _i64, _i32, _i32, _vp, _vp]),
 }
 

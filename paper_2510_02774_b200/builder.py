@@ -258,11 +258,9 @@ class _DevicePools:
         self.swap()
 
     def finalize(self, offsets: torch.Tensor, nbrs: torch.Tensor, bad: torch.Tensor) -> None:
-        _lib.call(
-            "grnnd_finalize", self.read_ids.data_ptr(), self.read_dists.data_ptr(), self.read_count.data_ptr(),
-            self.rows, self.cap, offsets.data_ptr(), nbrs.data_ptr(), bad.data_ptr(),
-            self.workspace.data_ptr(), self.workspace.numel(), _stream(self.dev),
-        )
+        p = self.struct()
+        _lib.call("grnnd_finalize_pools", C.byref(p), offsets.data_ptr(), nbrs.data_ptr(), bad.data_ptr(),
+                  _stream(self.dev))
 
     def sorted_rows(self) -> torch.Tensor:
         out = torch.empty((self.rows, self.cap), dtype=torch.int32, device=self.dev)

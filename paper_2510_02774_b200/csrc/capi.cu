@@ -449,7 +449,17 @@ int grnnd_finalize(const int32_t *ids, const float *dists, const int32_t *counts
     Workspace w;
     GRNND_TRY(check_ws(workspace, workspace_bytes, n, cap, 0, &w));
     GRNND_TRY(launch_scan_counts(counts, n, offsets, w.scan_tmp, S(s)));
-    return launch_finalize(ids, dists, counts, n, cap, offsets, nbrs, nullptr, bad_flag, S(s));
+    return launch_finalize(ids, dists, counts, n, cap, 0, n, offsets, nbrs, nullptr, bad_flag, S(s));
+}
+
+int grnnd_finalize_pools(const grnnd_pools *p, int64_t *offsets, int32_t *nbrs, int64_t *bad_flag,
+                         grnnd_stream_t s) {
+    Workspace w;
+    GRNND_TRY(pools_workspace(p, &w));
+    const int64_t n = p->hi - p->lo;
+    GRNND_TRY(launch_scan_counts(p->read_count, n, offsets, w.scan_tmp, S(s)));
+    return launch_finalize(p->read_ids, p->read_dists, p->read_count, n, p->cap, p->lo, p->n_total, offsets,
+                           nbrs, nullptr, bad_flag, S(s));
 }
 
 int grnnd_sorted_rows(const int32_t *ids, const float *dists, const int32_t *counts, int64_t n, int32_t cap,
@@ -458,7 +468,7 @@ int grnnd_sorted_rows(const int32_t *ids, const float *dists, const int32_t *cou
         set_error("cap %d unsupported", cap);
         return GRNND_EUNSUPPORTED;
     }
-    return launch_finalize(ids, dists, counts, n, cap, nullptr, nullptr, out_ids, nullptr, S(s));
+    return launch_finalize(ids, dists, counts, n, cap, 0, n, nullptr, nullptr, out_ids, nullptr, S(s));
 }
 
 int grnnd_check_finite(const float *data, int64_t n, int32_t dim, int32_t ld, int64_t *bad_flag, grnnd_stream_t s) {

@@ -89,7 +89,7 @@ int launch_init_dists(const float *data, int32_t dim, int32_t ld, int64_t lo, in
                       const int32_t *ids, int32_t ld_ids, int32_t count, float *out,
                       int32_t ld_out, cudaStream_t st);
 int launch_finalize(const int32_t *ids, const float *dists, const int32_t *counts, int64_t n,
-                    int32_t cap, const int64_t *offsets, int32_t *nbrs, int32_t *fixed_out,
-                    int64_t *bad_flag, cudaStream_t st);
+                    int32_t cap, int64_t lo, int64_t n_total, const int64_t *offsets, int32_t *nbrs,
+                    int32_t *fixed_out, int64_t *bad_flag, cudaStream_t st);
 
 }  // namespace grnnd

@@ -229,6 +229,7 @@ int launch_init_dists(const float *data, int32_t dim, int32_t ld, int64_t lo, in
 template <int RPL>
 __global__ void __launch_bounds__(256) finalize_kernel(const int32_t *__restrict__ ids, const float *__restrict__ dists,
                                                        const int32_t *__restrict__ counts, int64_t n, int32_t cap,
+                                                       int64_t lo, int64_t n_total,
                                                        const int64_t *__restrict__ offsets, int32_t *__restrict__ nbrs,
                                                        int32_t *__restrict__ fixed_out,
                                                        unsigned long long *__restrict__ bad) {
@@ -252,8 +253,8 @@ __global__ void __launch_bounds__(256) finalize_kernel(const int32_t *__restrict
         for (int r = 0; r < RPL; ++r) {
             const int s = r * 32 + lane;
             if (s < k) {
-                if (id[r] < 0 || id[r] >= n) flags |= 1ull;
-                if (id[r] == v) flags |= 2ull;
+                if (id[r] < 0 || id[r] >= n_total) flags |= 1ull;
+                if (id[r] == lo + v) flags |= 2ull;
                 if (nbrs) nbrs[offsets[v] + rank[r]] = id[r];
                 if (fixed_out) fixed_out[v * cap + rank[r]] = id[r];
             } else if (s < cap && fixed_out) {
@@ -265,19 +266,22 @@ __global__ void __launch_bounds__(256) finalize_kernel(const int32_t *__restrict
 }
 
 int launch_finalize(const int32_t *ids, const float *dists, const int32_t *counts, int64_t n, int32_t cap,
-                    const int64_t *offsets, int32_t *nbrs, int32_t *fixed_out, int64_t *bad_flag, cudaStream_t st) {
+                    int64_t lo, int64_t n_total, const int64_t *offsets, int32_t *nbrs, int32_t *fixed_out,
+                    int64_t *bad_flag, cudaStream_t st) {
     unsigned long long *bad = (unsigned long long *)bad_flag;
     if (n <= 0) return GRNND_OK;
     const unsigned g = warp_grid(n);
+#define GRNND_FIN(R) finalize_kernel<R><<<g, 256, 0, st>>>(ids, dists, counts, n, cap, lo, n_total, offsets, nbrs, fixed_out, bad)
     switch ((cap + 31) / 32) {
-        case 1: finalize_kernel<1><<<g, 256, 0, st>>>(ids, dists, counts, n, cap, offsets, nbrs, fixed_out, bad); break;
-        case 2: finalize_kernel<2><<<g, 256, 0, st>>>(ids, dists, counts, n, cap, offsets, nbrs, fixed_out, bad); break;
-        case 3: finalize_kernel<3><<<g, 256, 0, st>>>(ids, dists, counts, n, cap, offsets, nbrs, fixed_out, bad); break;
-        case 4: finalize_kernel<4><<<g, 256, 0, st>>>(ids, dists, counts, n, cap, offsets, nbrs, fixed_out, bad); break;
-        case 5: finalize_kernel<5><<<g, 256, 0, st>>>(ids, dists, counts, n, cap, offsets, nbrs, fixed_out, bad); break;
-        case 6: finalize_kernel<6><<<g, 256, 0, st>>>(ids, dists, counts, n, cap, offsets, nbrs, fixed_out, bad); break;
-        case 7: finalize_kernel<7><<<g, 256, 0, st>>>(ids, dists, counts, n, cap, offsets, nbrs, fixed_out, bad); break;
-        case 8: finalize_kernel<8><<<g, 256, 0, st>>>(ids, dists, counts, n, cap, offsets, nbrs, fixed_out, bad); break;
+        case 1: GRNND_FIN(1); break;
+        case 2: GRNND_FIN(2); break;
+        case 3: GRNND_FIN(3); break;
+        case 4: GRNND_FIN(4); break;
+        case 5: GRNND_FIN(5); break;
+        case 6: GRNND_FIN(6); break;
+        case 7: GRNND_FIN(7); break;
+        case 8: GRNND_FIN(8); break;
+#undef GRNND_FIN
         default: set_error("cap %d > %d unsupported", cap, GRNND_MAX_CAP); return GRNND_EUNSUPPORTED;
     }
     return check_launch("finalize_kernel");
