@@ -8,11 +8,14 @@ be loaded, importing this module raises.  Build it with
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from .errors import DeviceError, ParamError
 
 LIB_PATH = Path(__file__).resolve().parent / "_build" / "libgrnnd_b200.so"
+if os.environ.get("GRNND_B200_LIB"):  # A/B builds of the same sources (tools/variants.sh)
+    LIB_PATH = Path(os.environ["GRNND_B200_LIB"]).resolve()
 
 OK, EINVAL, ECUDA, EUNSUPPORTED, EWORKSPACE = 0, 1, 2, 3, 4
 NSTATS = 16

@@ -41,6 +41,12 @@ struct Workspace {
     int32_t *heavy;      // [n] heavy segment ids
     uint8_t *pos8;       // [n, cap] permutation position of each pool slot (this round)
     int32_t cap;
+    int32_t mw;          // 64-bit words per mask row = ceil(cap / 64)
+    uint64_t *cond;      // [n, cap, mw] redirect-condition bits, row = anchor position
+    uint64_t *afar;      // [n, cap, mw] "anchor is the farther member" bits
+    int32_t *cl_n;       // [n] redirect-capable pairs found (may exceed the list)
+    uint32_t *cl;        // [n, 4*cap] (key << 16 | ...) packed: key in high 16 bits of the slot
+    float *cl_d;         // [n, 4*cap] their exact distances
     int64_t n;
     int64_t msg_capacity;
 };
@@ -82,6 +88,12 @@ inline size_t carve(Workspace *w, void *base, int64_t n, int32_t cap, int64_t ms
     t.heavy = (int32_t *)take(4 * N);
     t.pos8 = (uint8_t *)take(N * (size_t)(cap > 0 ? cap : 1));
     t.cap = cap;
+    t.mw = (cap + 63) / 64 > 0 ? (cap + 63) / 64 : 1;
+    t.cond = (uint64_t *)take(8 * N * (size_t)(cap > 0 ? cap : 1) * (size_t)t.mw);
+    t.afar = (uint64_t *)take(8 * N * (size_t)(cap > 0 ? cap : 1) * (size_t)t.mw);
+    t.cl_n = (int32_t *)take(4 * N);
+    t.cl = (uint32_t *)take(4 * N * 4 * (size_t)(cap > 0 ? cap : 1));
+    t.cl_d = (float *)take(4 * N * 4 * (size_t)(cap > 0 ? cap : 1));
     t.n = n;
     t.msg_capacity = msg_capacity;
     if (w) *w = t;
