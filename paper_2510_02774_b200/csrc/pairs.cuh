@@ -1,0 +1,304 @@
+// pairs.cuh -- the order-free FP32 hot loop of the pair phase (included by propagate.cu,
+// inside namespace grnnd, after row_stride16 / tile_decode / tile_accumulate).
+//
+// A CTA processes a BATCH of B pools at a time (B = 4 for k <= 16, 2 for k <= 32, else 1):
+// the pools' rows share one shared-memory slab and their TxT tiles share one thread
+// loop, so small pools (most of them: the median k is ~13) still keep every lane busy
+// and amortise the gather latency and barriers over B vertices.  The next batch's rows
+// are gathered (cp.async) while this batch's masks are written out.
+#pragma once
+
+template <int MAXK, int B>
+struct PairSmem {
+    static constexpr int W = (MAXK + 63) / 64;  // 64-bit words per mask row
+    static constexpr int CL = 4 * MAXK;         // redirect-capable pairs whose distance is kept
+    uint64_t cond[B][MAXK * W];
+    uint64_t afar[B][MAXK * W];
+    int32_t ids[2][B][MAXK];  // pool rows of the current / next batch
+    float dv[2][B][MAXK];
+    int32_t pos[2][B][MAXK];  // slot -> permutation position
+    int32_t k[2][B];
+    int64_t v[2][B];          // local row of each batch member (-1: none)
+    uint32_t cl_key[B][CL];   // (anchor pos << 8) | partner pos
+    float cl_d[B][CL];
+    int cl_n[B];
+    int tp[B + 1];            // tile prefix over the batch members
+};
+
+// redirect condition of the T*T pairs of tile (bI, bJ) of member g, as bits in
+// permutation space, plus the distance of each redirect-capable pair
+template <int MAXK, int B, int T>
+__device__ __forceinline__ unsigned tile_epilogue(PairSmem<MAXK, B> &sm, int cur, int g, const float (&acc)[T * T],
+                                                  int bI, int bJ, int nb, int k) {
+    using S = PairSmem<MAXK, B>;
+    constexpr int W = S::W;
+    // the tile's 2T pool entries once (not per pair); the common "no redirect" outcome is
+    // branch free, only redirect-capable pairs (~0.02% of pairs) take the atomic path
+    float dA[T], dB[T];
+    bool vA[T], vB[T];
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+        const int s = bI + nb * i, u = bJ + nb * i;
+        vA[i] = s < k && sm.ids[cur][g][s] != TOMB;
+        vB[i] = u < k && sm.ids[cur][g][u] != TOMB;
+        dA[i] = vA[i] ? sm.dv[cur][g][s] : 0.0f;
+        dB[i] = vB[i] ? sm.dv[cur][g][u] : 0.0f;
+    }
+    unsigned npairs = 0;
+#pragma unroll
+    for (int i = 0; i < T; ++i)
+#pragma unroll
+        for (int j = 0; j < T; ++j) {
+            const int s = bI + nb * i, u = bJ + nb * j;
+            // off-diagonal tiles hold each unordered pair once; diagonal ones twice
+            const bool valid = vA[i] && vB[j] && (bI != bJ || i < j);
+            npairs += valid ? 1u : 0u;
+            const float d1 = dA[i], d2 = dB[j];
+            const float hi = d1 >= d2 ? d1 : d2;
+            if (valid && acc[i * T + j] < hi) {
+                {
+                    const int x1 = sm.pos[cur][g][s], x2 = sm.pos[cur][g][u];
+                    // anchor = the member visited first (smaller position)
+                    const int xa = x1 < x2 ? x1 : x2, xb = x1 < x2 ? x2 : x1;
+                    const float dva = x1 < x2 ? d1 : d2, dvb = x1 < x2 ? d2 : d1;
+                    const unsigned long long bit = 1ull << (xb & 63);
+                    atomicOr((unsigned long long *)&sm.cond[g][xa * W + (xb >> 6)], bit);
+                    if (!(dvb >= dva)) atomicOr((unsigned long long *)&sm.afar[g][xa * W + (xb >> 6)], bit);
+                    const int c = atomicAdd(&sm.cl_n[g], 1);
+                    if (c < S::CL) {
+                        sm.cl_key[g][c] = (uint32_t)((xa << 8) | xb);
+                        sm.cl_d[g][c] = acc[i * T + j];
+                    }
+                }
+            }
+        }
+    return npairs;
+}
+
+// MULTI: D > 128, rows staged 128 dims at a time with accumulators held across chunks
+// (always B = 1).
+template <int MAXK, int B, int THREADS, int TPT, int T, bool MULTI, int NQ>
+__global__ void __launch_bounds__(THREADS) pairs_kernel(PropArgs a, int bin, int kmax) {
+    using S = PairSmem<MAXK, B>;
+    constexpr int W = S::W;
+    constexpr int PER = (B * MAXK + THREADS - 1) / THREADS;  // pool slots per thread
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    S &sm = *reinterpret_cast<S *>(smem_raw);
+    float4 *rows = reinterpret_cast<float4 *>(smem_raw + align_up(sizeof(S), 128));
+
+    const int tid = threadIdx.x;
+    const int64_t nbin = (int64_t)a.w.ctr[C_BIN0 + bin];
+    const int64_t nbatch = (nbin + B - 1) / B;
+    const int32_t *blist = a.w.bins + (int64_t)bin * a.w.n;
+    const int nq_total = (a.dim + 3) >> 2;  // float4 per row (ld % 4 == 0, pad cols are 0)
+    const int rs4 = row_stride16(nq_total);
+    const int nchunks = (nq_total + DC4 - 1) / DC4;
+    const int cap = a.cap;
+    const int mw = a.w.mw;
+    unsigned long long pairs_local = 0;
+
+    int32_t nid[PER];
+    float ndv[PER];
+    int32_t npos[PER];
+    int nk[PER];
+    int64_t nv[PER];
+    auto fetch_meta = [&](int64_t bi) {  // next batch's pool rows -> registers
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int e = r * THREADS + tid;
+            const int g = e / MAXK, s = e - g * MAXK;
+            nk[r] = 0;
+            nv[r] = -1;
+            if (g < B && bi * B + g < nbin) {
+                const int64_t v = blist[bi * B + g];
+                const int k = a.read_count[v];
+                nv[r] = v;
+                nk[r] = k;
+                if (s < k) {
+                    nid[r] = a.read_ids[v * cap + s];
+                    ndv[r] = a.read_dists[v * cap + s];
+                    npos[r] = a.order_code == 0 ? (int32_t)a.w.pos8[v * cap + s] : 0;
+                }
+            }
+        }
+    };
+    auto store_meta = [&](int slot) {
+#pragma unroll
+        for (int r = 0; r < PER; ++r) {
+            const int e = r * THREADS + tid;
+            const int g = e / MAXK, s = e - g * MAXK;
+            if (g < B) {
+                if (s < nk[r]) {
+                    sm.ids[slot][g][s] = nid[r];
+                    sm.dv[slot][g][s] = ndv[r];
+                    sm.pos[slot][g][s] = npos[r];
+                }
+                if (s == 0) {
+                    sm.k[slot][g] = nk[r];
+                    sm.v[slot][g] = nv[r];
+                }
+            }
+        }
+    };
+    auto load_rows = [&](int slot, int c) {  // chunk c of every member's rows (cp.async)
+        const int q0 = c * DC4;
+        const int nq = min(DC4, nq_total - q0);
+#pragma unroll
+        for (int g = 0; g < B; ++g) {
+            const int k = sm.k[slot][g];
+            const int total = k * nq;
+            for (int e = tid; e < total; e += THREADS) {
+                const int r = e / nq;
+                const int q = e - r * nq;
+                const int32_t id = sm.ids[slot][g][r];
+                const float *src = a.data + (int64_t)(id < 0 ? 0 : id) * a.ld + (int64_t)(q0 + q) * 4;
+                cp_async16(&rows[(g * kmax + r) * rs4 + q], src, id >= 0);
+            }
+        }
+        cp_async_commit();
+    };
+
+    int64_t bi = blockIdx.x;
+    if (bi >= nbatch) return;
+    fetch_meta(bi);
+    store_meta(0);
+    __syncthreads();
+    if (!MULTI) load_rows(0, 0);
+    int cur = 0;
+
+    for (; bi < nbatch; bi += gridDim.x) {
+        const int64_t bi_next = bi + gridDim.x;
+        const bool has_next = bi_next < nbatch;
+
+        if (a.order_code != 0) {
+            // ascending debug order (:75-87): stable rank by (dist, id); published for decide
+#pragma unroll
+            for (int g = 0; g < B; ++g) {
+                const int k = sm.k[cur][g];
+                for (int s = tid; s < k; s += THREADS) {
+                    const float ds = sm.dv[cur][g][s];
+                    const int32_t is = sm.ids[cur][g][s];
+                    int r = 0;
+                    for (int t = 0; t < k; ++t) {
+                        const float dt = sm.dv[cur][g][t];
+                        const int32_t it2 = sm.ids[cur][g][t];
+                        r += (dt < ds || (dt == ds && (it2 < is || (it2 == is && t < s)))) ? 1 : 0;
+                    }
+                    sm.pos[cur][g][s] = r;
+                    a.w.pos8[sm.v[cur][g] * cap + s] = (uint8_t)r;
+                }
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < B; ++g) {
+            const int k = sm.k[cur][g];
+            for (int i = tid; i < k * W; i += THREADS) {
+                sm.cond[g][i] = 0ull;
+                sm.afar[g][i] = 0ull;
+            }
+        }
+        if (tid == 0) {
+            int t = 0;
+#pragma unroll
+            for (int g = 0; g < B; ++g) {
+                sm.cl_n[g] = 0;
+                sm.tp[g] = t;
+                const int nb = (sm.k[cur][g] + T - 1) / T;
+                t += nb * (nb + 1) / 2;
+            }
+            sm.tp[B] = t;
+        }
+        if (has_next) fetch_meta(bi_next);
+
+        if (!MULTI) {
+            cp_async_wait_all();
+            __syncthreads();  // rows landed; masks zeroed; tile prefix visible
+            const int ntiles = sm.tp[B];
+            for (int t = tid; t < ntiles; t += THREADS) {
+                int g = 0;
+#pragma unroll
+                for (int h = 1; h < B; ++h) g += t >= sm.tp[h] ? 1 : 0;
+                int bI, bJ;
+                tile_decode(t - sm.tp[g], bI, bJ);
+                float acc[T * T];
+#pragma unroll
+                for (int p = 0; p < T * T; ++p) acc[p] = 0.0f;
+                const int r0 = g * kmax;
+                const int kg = sm.k[cur][g];
+                const int nb = (kg + T - 1) / T;
+                tile_accumulate<T, NQ>(acc, rows, r0 + bI, r0 + bJ, nb, nq_total, rs4);
+                pairs_local += tile_epilogue<MAXK, B, T>(sm, cur, g, acc, bI, bJ, nb, kg);
+            }
+            if (has_next) store_meta(cur ^ 1);
+            __syncthreads();  // masks complete; row slab free; next pool rows visible
+            if (has_next) load_rows(cur ^ 1, 0);  // lands while the masks are written out
+        } else {
+            const int k = sm.k[cur][0];
+            const int nb = (k + T - 1) / T;
+            const int ntiles = nb * (nb + 1) / 2;
+            __syncthreads();
+            for (int g0 = 0; g0 < ntiles; g0 += THREADS * TPT) {
+                float acc[TPT][T * T];
+#pragma unroll
+                for (int tt = 0; tt < TPT; ++tt)
+#pragma unroll
+                    for (int p = 0; p < T * T; ++p) acc[tt][p] = 0.0f;
+                for (int c = 0; c < nchunks; ++c) {
+                    __syncthreads();  // everyone done with the previous chunk
+                    load_rows(cur, c);
+                    cp_async_wait_all();
+                    __syncthreads();
+                    const int nq = min(DC4, nq_total - c * DC4);
+#pragma unroll
+                    for (int tt = 0; tt < TPT; ++tt) {
+                        const int t = g0 + tt * THREADS + tid;
+                        if (t < ntiles) {
+                            int bI, bJ;
+                            tile_decode(t, bI, bJ);
+                            tile_accumulate<T, 0>(acc[tt], rows, bI, bJ, nb, nq, rs4);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int tt = 0; tt < TPT; ++tt) {
+                    const int t = g0 + tt * THREADS + tid;
+                    if (t < ntiles) {
+                        int bI, bJ;
+                        tile_decode(t, bI, bJ);
+                        pairs_local += tile_epilogue<MAXK, B, T>(sm, cur, 0, acc[tt], bI, bJ, nb, k);
+                    }
+                }
+            }
+            if (has_next) store_meta(cur ^ 1);
+            __syncthreads();
+        }
+        // masks + kept distances -> global (decide_kernel)
+#pragma unroll
+        for (int g = 0; g < B; ++g) {
+            const int64_t v = sm.v[cur][g];
+            if (v < 0) continue;
+            const int k = sm.k[cur][g];
+            uint64_t *gc = a.w.cond + v * (int64_t)cap * mw;
+            uint64_t *ga = a.w.afar + v * (int64_t)cap * mw;
+            for (int e = tid; e < (k - 1) * mw; e += THREADS) {
+                const int x = e / mw, wd = e - x * mw;
+                gc[e] = wd < W ? sm.cond[g][x * W + wd] : 0ull;
+                ga[e] = wd < W ? sm.afar[g][x * W + wd] : 0ull;
+            }
+            const int lcap = 4 * (MAXK < cap ? MAXK : cap);
+            const int ncl = sm.cl_n[g];
+            const int nw = ncl < lcap ? ncl : lcap;
+            if (tid == 0) a.w.cl_n[v] = nw;  // truncated lists: decide re-evaluates misses
+            for (int e = tid; e < nw; e += THREADS) {
+                a.w.cl[v * 4 * (int64_t)cap + e] = sm.cl_key[g][e];
+                a.w.cl_d[v * 4 * (int64_t)cap + e] = sm.cl_d[g][e];
+            }
+        }
+        __syncthreads();  // per-batch shared state is reused next iteration
+        cur ^= 1;
+    }
+    if (a.stats) {
+        pairs_local = warp_sum(pairs_local);
+        if (lane_id() == 0 && pairs_local) atomicAdd((unsigned long long *)&a.stats[GRNND_ST_PAIRS], pairs_local);
+    }
+}

@@ -33,12 +33,11 @@ __device__ __forceinline__ int bin_of(int k) {
 }
 
 constexpr int DC4 = 32;  // float4 per row chunk (128 dims)
-#ifndef GRNND_NBUF
-#define GRNND_NBUF 1  // row buffers per pairs CTA (2 = cross-vertex prefetch, half the CTAs/SM)
+#ifndef GRNND_B1_BATCH
+#define GRNND_B1_BATCH 4  // pools per CTA batch, k <= 16
 #endif
-#ifndef GRNND_BIN3_T
-#define GRNND_BIN3_T 2
-#define GRNND_BIN3_THREADS 128
+#ifndef GRNND_B2_BATCH
+#define GRNND_B2_BATCH 2  // pools per CTA batch, k <= 32
 #endif
 
 // ---------------------------------------------------------------------------------
@@ -116,11 +115,13 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool va
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
-// row r, float4 column q -> swizzled float4 index: lanes reading the same q of rows
-// T*b + i for consecutive b hit distinct 16-byte bank groups
-template <int T>
-__device__ __forceinline__ int swz(int r, int q, int rs4) {
-    return r * rs4 + (q ^ ((r / T) & 7));
+// Row staging: row r's float4 column q at r * rs4 + q with an ODD row stride rs4 (in
+// 16-byte units), and strided tiles (tile (bI, bJ) = rows bI + nb*i x bJ + nb*j), so the
+// 8 lanes of an LDS.128 phase -- consecutive bI -- read 8 consecutive rows: every 16-byte
+// bank group once, conflict free without any swizzle arithmetic in the inner loop.
+__host__ __device__ __forceinline__ int row_stride16(int nq_total) {
+    const int c = nq_total < 32 ? nq_total : 32;
+    return c | 1;
 }
 
 // upper-triangle tile index t (bJ-major) -> (bI, bJ), bI <= bJ
@@ -132,31 +133,25 @@ __device__ __forceinline__ void tile_decode(int t, int &bI, int &bJ) {
     bI = t - j * (j + 1) / 2;
 }
 
-template <int MAXK>
-struct PairSmem {
-    static constexpr int W = (MAXK + 63) / 64;  // 64-bit words per mask row
-    uint64_t cond[MAXK * W];
-    uint64_t afar[MAXK * W];
-    int32_t ids[2][MAXK];  // pool rows of the current / next vertex
-    float dv[2][MAXK];
-    int32_t pos[2][MAXK];  // slot -> permutation position
-    static constexpr int CL = 4 * MAXK;  // redirect-capable pairs whose distance is kept
-    uint32_t cl_key[CL];   // (anchor pos << 8) | partner pos
-    float cl_d[CL];
-    int cl_n;
-};
-
-// T*T exact accumulators of a TxT tile over float4 columns [q0, q1)
-template <int T>
+// T*T exact accumulators of tile (rows rA + nb*i) x (rows rB + nb*j) over float4 columns
+// [0, nq); NQ > 0 fixes the trip count at compile time (D = 128: 32 columns)
+template <int T, int NQ>
 __device__ __forceinline__ void tile_accumulate(float (&acc)[T * T], const float4 *__restrict__ rows, int rA, int rB,
-                                                int q0, int q1, int rs4) {
-#pragma unroll 2
-    for (int q = q0; q < q1; ++q) {
+                                                int nb, int nq, int rs4) {
+    const float4 *pa[T], *pb[T];
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+        pa[i] = rows + (rA + nb * i) * rs4;
+        pb[i] = rows + (rB + nb * i) * rs4;
+    }
+    const int n = NQ > 0 ? NQ : nq;
+#pragma unroll 4
+    for (int q = 0; q < n; ++q) {
         float4 A[T], B[T];
 #pragma unroll
-        for (int i = 0; i < T; ++i) A[i] = rows[swz<T>(rA + i, q, rs4)];
+        for (int i = 0; i < T; ++i) A[i] = pa[i][q];
 #pragma unroll
-        for (int j = 0; j < T; ++j) B[j] = rows[swz<T>(rB + j, q, rs4)];
+        for (int j = 0; j < T; ++j) B[j] = pb[j][q];
 #pragma unroll
         for (int i = 0; i < T; ++i)
 #pragma unroll
@@ -171,223 +166,7 @@ __device__ __forceinline__ void tile_accumulate(float (&acc)[T * T], const float
     }
 }
 
-// redirect condition of the T*T pairs of tile (bI, bJ), as bits in permutation space
-template <int MAXK, int T>
-__device__ __forceinline__ unsigned tile_epilogue(PairSmem<MAXK> &sm, int cur, const float (&acc)[T * T], int bI,
-                                                  int bJ, int k) {
-    constexpr int W = PairSmem<MAXK>::W;
-    unsigned npairs = 0;
-#pragma unroll
-    for (int i = 0; i < T; ++i)
-#pragma unroll
-        for (int j = 0; j < T; ++j) {
-            const int s = bI * T + i, u = bJ * T + j;
-            if (s < u && u < k && sm.ids[cur][s] != TOMB && sm.ids[cur][u] != TOMB) {
-                ++npairs;
-                const float d1 = sm.dv[cur][s], d2 = sm.dv[cur][u];
-                const float hi = d1 >= d2 ? d1 : d2;
-                if (acc[i * T + j] < hi) {
-                    const int x1 = sm.pos[cur][s], x2 = sm.pos[cur][u];
-                    // anchor = the member visited first (smaller position)
-                    const int xa = x1 < x2 ? x1 : x2, xb = x1 < x2 ? x2 : x1;
-                    const float dva = x1 < x2 ? d1 : d2, dvb = x1 < x2 ? d2 : d1;
-                    const unsigned long long bit = 1ull << (xb & 63);
-                    atomicOr((unsigned long long *)&sm.cond[xa * W + (xb >> 6)], bit);
-                    if (!(dvb >= dva)) atomicOr((unsigned long long *)&sm.afar[xa * W + (xb >> 6)], bit);
-                    const int c = atomicAdd(&sm.cl_n, 1);
-                    if (c < PairSmem<MAXK>::CL) {
-                        sm.cl_key[c] = (uint32_t)((xa << 8) | xb);
-                        sm.cl_d[c] = acc[i * T + j];
-                    }
-                }
-            }
-        }
-    return npairs;
-}
-
-// MULTI: D > 128, rows staged 128 dims at a time with accumulators held across chunks.
-// NBUF: 2 = the next vertex's rows are gathered while this vertex computes.
-template <int MAXK, int THREADS, int TPT, int T, bool MULTI, int NBUF>
-__global__ void __launch_bounds__(THREADS) pairs_kernel(PropArgs a, int bin, int kmax) {
-    using S = PairSmem<MAXK>;
-    constexpr int W = S::W;
-    constexpr int PER = (MAXK + THREADS - 1) / THREADS;  // pool slots per thread
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    S &sm = *reinterpret_cast<S *>(smem_raw);
-    float4 *rows0 = reinterpret_cast<float4 *>(smem_raw + align_up(sizeof(S), 128));
-
-    const int tid = threadIdx.x;
-    const int64_t nbin = (int64_t)a.w.ctr[C_BIN0 + bin];
-    const int32_t *blist = a.w.bins + (int64_t)bin * a.w.n;
-    const int nq_total = (a.dim + 3) >> 2;  // float4 per row (ld % 4 == 0, pad cols are 0)
-    const int rs4 = nq_total >= DC4 ? DC4 : ((nq_total + 7) & ~7);
-    const int nchunks = (nq_total + DC4 - 1) / DC4;
-    const int cap = a.cap;
-    const int mw = a.w.mw;
-    const int buf_elems = kmax * rs4;
-    unsigned long long pairs_local = 0;
-
-    int32_t nid[PER];
-    float ndv[PER];
-    int32_t npos[PER];
-    auto fetch_meta = [&](int64_t it) {  // next vertex's pool row -> registers
-        const int64_t v = blist[it];
-        const int k = a.read_count[v];
-#pragma unroll
-        for (int r = 0; r < PER; ++r) {
-            const int s = r * THREADS + tid;
-            if (s < k) {
-                nid[r] = a.read_ids[v * cap + s];
-                ndv[r] = a.read_dists[v * cap + s];
-                npos[r] = a.order_code == 0 ? (int32_t)a.w.pos8[v * cap + s] : 0;
-            }
-        }
-        return k;
-    };
-    auto store_meta = [&](int slot, int k) {
-#pragma unroll
-        for (int r = 0; r < PER; ++r) {
-            const int s = r * THREADS + tid;
-            if (s < k) {
-                sm.ids[slot][s] = nid[r];
-                sm.dv[slot][s] = ndv[r];
-                sm.pos[slot][s] = npos[r];
-            }
-        }
-    };
-    auto load_rows = [&](float4 *rows, int slot, int k, int c) {
-        const int q0 = c * DC4;
-        const int nq = min(DC4, nq_total - q0);
-        const int total = k * nq;
-        for (int e = tid; e < total; e += THREADS) {
-            const int r = e / nq;
-            const int q = e - r * nq;
-            const int32_t id = sm.ids[slot][r];
-            const float *src = a.data + (int64_t)(id < 0 ? 0 : id) * a.ld + (int64_t)(q0 + q) * 4;
-            cp_async16(&rows[swz<T>(r, q, rs4)], src, id >= 0);
-        }
-        cp_async_commit();
-    };
-
-    int64_t it = blockIdx.x;
-    if (it >= nbin) return;
-    int kn = fetch_meta(it);
-    store_meta(0, kn);
-    __syncthreads();
-    if (!MULTI) load_rows(rows0, 0, kn, 0);
-    int cur = 0;
-
-    for (; it < nbin; it += gridDim.x) {
-        const int64_t v = blist[it];
-        const int k = kn;
-        const int64_t it_next = it + gridDim.x;
-        const bool has_next = it_next < nbin;
-        float4 *rows = rows0 + (NBUF == 2 ? cur * buf_elems : 0);
-        float4 *rows_next = rows0 + (NBUF == 2 ? (cur ^ 1) * buf_elems : 0);
-
-        if (a.order_code != 0) {
-            // ascending debug order (:75-87): stable rank by (dist, id); published for decide
-            for (int s = tid; s < k; s += THREADS) {
-                const float ds = sm.dv[cur][s];
-                const int32_t is = sm.ids[cur][s];
-                int r = 0;
-                for (int t = 0; t < k; ++t) {
-                    const float dt = sm.dv[cur][t];
-                    const int32_t it2 = sm.ids[cur][t];
-                    r += (dt < ds || (dt == ds && (it2 < is || (it2 == is && t < s)))) ? 1 : 0;
-                }
-                sm.pos[cur][s] = r;
-                a.w.pos8[v * cap + s] = (uint8_t)r;
-            }
-        }
-        for (int i = tid; i < k * W; i += THREADS) {
-            sm.cond[i] = 0ull;
-            sm.afar[i] = 0ull;
-        }
-        if (tid == 0) sm.cl_n = 0;
-        if (has_next) kn = fetch_meta(it_next);
-        const int nb = (k + T - 1) / T;
-        const int ntiles = nb * (nb + 1) / 2;
-        if (!MULTI) {
-            cp_async_wait_all();
-            if (NBUF == 2 && has_next) store_meta(cur ^ 1, kn);
-            __syncthreads();  // rows(v) landed; masks zeroed; next pool row visible
-            if (NBUF == 2 && has_next) load_rows(rows_next, cur ^ 1, kn, 0);
-            for (int t = tid; t < ntiles; t += THREADS) {
-                int bI, bJ;
-                tile_decode(t, bI, bJ);
-                float acc[T * T];
-#pragma unroll
-                for (int p = 0; p < T * T; ++p) acc[p] = 0.0f;
-                tile_accumulate<T>(acc, rows, bI * T, bJ * T, 0, nq_total, rs4);
-                pairs_local += tile_epilogue<MAXK, T>(sm, cur, acc, bI, bJ, k);
-            }
-            if (NBUF == 1 && has_next) store_meta(cur ^ 1, kn);
-            __syncthreads();  // masks complete; single buffer free
-            if (NBUF == 1 && has_next) load_rows(rows0, cur ^ 1, kn, 0);
-        } else {
-            __syncthreads();
-            for (int g0 = 0; g0 < ntiles; g0 += THREADS * TPT) {
-                float acc[TPT][T * T];
-#pragma unroll
-                for (int tt = 0; tt < TPT; ++tt)
-#pragma unroll
-                    for (int p = 0; p < T * T; ++p) acc[tt][p] = 0.0f;
-                for (int c = 0; c < nchunks; ++c) {
-                    __syncthreads();  // everyone done with the previous chunk
-                    load_rows(rows0, cur, k, c);
-                    cp_async_wait_all();
-                    __syncthreads();
-                    const int nq = min(DC4, nq_total - c * DC4);
-#pragma unroll
-                    for (int tt = 0; tt < TPT; ++tt) {
-                        const int t = g0 + tt * THREADS + tid;
-                        if (t < ntiles) {
-                            int bI, bJ;
-                            tile_decode(t, bI, bJ);
-                            tile_accumulate<T>(acc[tt], rows0, bI * T, bJ * T, 0, nq, rs4);
-                        }
-                    }
-                }
-#pragma unroll
-                for (int tt = 0; tt < TPT; ++tt) {
-                    const int t = g0 + tt * THREADS + tid;
-                    if (t < ntiles) {
-                        int bI, bJ;
-                        tile_decode(t, bI, bJ);
-                        pairs_local += tile_epilogue<MAXK, T>(sm, cur, acc[tt], bI, bJ, k);
-                    }
-                }
-            }
-            if (has_next) store_meta(cur ^ 1, kn);
-            __syncthreads();
-        }
-        // masks -> global, rows of anchor positions 0..k-2 (coalesced words)
-        uint64_t *gc = a.w.cond + v * (int64_t)cap * mw;
-        uint64_t *ga = a.w.afar + v * (int64_t)cap * mw;
-        for (int e = tid; e < (k - 1) * mw; e += THREADS) {
-            const int x = e / mw, wd = e - x * mw;
-            gc[e] = wd < W ? sm.cond[x * W + wd] : 0ull;
-            ga[e] = wd < W ? sm.afar[x * W + wd] : 0ull;
-        }
-        {  // distances of the redirect-capable pairs (looked up by decide_kernel)
-            const int lcap = 4 * (MAXK < cap ? MAXK : cap);
-            const int ncl = sm.cl_n;
-            const int nw = ncl < lcap ? ncl : lcap;
-            if (tid == 0) a.w.cl_n[v] = nw;  // truncated lists: decide re-evaluates misses
-            for (int e = tid; e < nw; e += THREADS) {
-                a.w.cl[v * 4 * (int64_t)cap + e] = sm.cl_key[e];
-                a.w.cl_d[v * 4 * (int64_t)cap + e] = sm.cl_d[e];
-            }
-        }
-        __syncthreads();  // masks / pool row of this vertex are reused next iteration
-        cur ^= 1;
-    }
-    if (a.stats) {
-        pairs_local = warp_sum(pairs_local);
-        if (lane_id() == 0 && pairs_local) atomicAdd((unsigned long long *)&a.stats[GRNND_ST_PAIRS], pairs_local);
-    }
-}
+#include "pairs.cuh"
 
 // ---------------------------------------------------------------------------------
 // 3. decide kernel: anchor-serial rule over the masks, emission, tombstones
@@ -632,14 +411,14 @@ static int sm_count() {
     return s;
 }
 
-template <int MAXK, int THREADS, int TPT, int T, bool MULTI, int NBUF>
+template <int MAXK, int B, int THREADS, int TPT, int T, bool MULTI, int NQ>
 static int launch_pairs_impl(const PropArgs &a, int bin, cudaStream_t st) {
-    auto kern = pairs_kernel<MAXK, THREADS, TPT, T, MULTI, NBUF>;
-    // TxT tiles read rows up to round_up(k, T) - 1: size each slab for that
+    auto kern = pairs_kernel<MAXK, B, THREADS, TPT, T, MULTI, NQ>;
+    // TxT tiles read rows up to round_up(k, T) - 1: size each member's slab for that
     const int kmax = ((MAXK < a.cap ? MAXK : a.cap) + T - 1) / T * T;
     const int nq_total = (a.dim + 3) >> 2;
-    const int rs4 = nq_total >= DC4 ? DC4 : ((nq_total + 7) & ~7);
-    const size_t smem = align_up(sizeof(PairSmem<MAXK>), 128) + (size_t)NBUF * kmax * rs4 * 16;
+    const int rs4 = row_stride16(nq_total);
+    const size_t smem = align_up(sizeof(PairSmem<MAXK, B>), 128) + (size_t)B * kmax * rs4 * 16;
     static int configured_smem = 0;
     if ((int)smem > configured_smem) {
         GRNND_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -655,10 +434,13 @@ static int launch_pairs_impl(const PropArgs &a, int bin, cudaStream_t st) {
     return check_launch("pairs_kernel");
 }
 
-template <int MAXK, int THREADS, int TPT, int T>
+// (MAXK, batch B, threads, tiles/thread kept across 128-dim chunks when D > 128, tile edge T)
+template <int MAXK, int B, int THREADS, int TPT, int T>
 static int launch_pairs(const PropArgs &a, int bin, cudaStream_t st) {
-    if (a.dim <= DC4 * 4) return launch_pairs_impl<MAXK, THREADS, TPT, T, false, GRNND_NBUF>(a, bin, st);
-    return launch_pairs_impl<MAXK, THREADS, TPT, T, true, 1>(a, bin, st);
+    const int nq_total = (a.dim + 3) >> 2;
+    if (nq_total == DC4) return launch_pairs_impl<MAXK, B, THREADS, TPT, T, false, DC4>(a, bin, st);
+    if (a.dim <= DC4 * 4) return launch_pairs_impl<MAXK, B, THREADS, TPT, T, false, 0>(a, bin, st);
+    return launch_pairs_impl<MAXK, 1, THREADS, TPT, T, true, 0>(a, bin, st);
 }
 
 int launch_propagate(const PropArgs &a, cudaStream_t st) {
@@ -672,11 +454,11 @@ int launch_propagate(const PropArgs &a, cudaStream_t st) {
                                                             a.msg_cnt);
     GRNND_TRY(check_launch("bin_kernel"));
     // largest k first so long CTAs start early
-    if (a.cap > 128) GRNND_TRY((launch_pairs<256, 256, 3, 4>(a, 5, st)));
-    if (a.cap > 64) GRNND_TRY((launch_pairs<128, 128, 3, 4>(a, 4, st)));
-    if (a.cap > 32) GRNND_TRY((launch_pairs<64, GRNND_BIN3_THREADS, 3, GRNND_BIN3_T>(a, 3, st)));
-    if (a.cap > 16) GRNND_TRY((launch_pairs<32, 64, 3, 2>(a, 2, st)));
-    if (a.cap > 1) GRNND_TRY((launch_pairs<16, 32, 2, 2>(a, 1, st)));
+    if (a.cap > 128) GRNND_TRY((launch_pairs<256, 1, 256, 3, 4>(a, 5, st)));
+    if (a.cap > 64) GRNND_TRY((launch_pairs<128, 1, 128, 3, 4>(a, 4, st)));
+    if (a.cap > 32) GRNND_TRY((launch_pairs<64, 1, 128, 3, 2>(a, 3, st)));
+    if (a.cap > 16) GRNND_TRY((launch_pairs<32, GRNND_B2_BATCH, 128, 3, 2>(a, 2, st)));
+    if (a.cap > 1) GRNND_TRY((launch_pairs<16, GRNND_B1_BATCH, 128, 2, 2>(a, 1, st)));
     const int64_t blocks = std::min<int64_t>((n + DEC_WARPS - 1) / DEC_WARPS, (int64_t)sm_count() * 16);
     const unsigned g = (unsigned)std::max<int64_t>(1, blocks);
     switch (a.w.mw) {
