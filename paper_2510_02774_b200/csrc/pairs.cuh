@@ -11,12 +11,12 @@
 template <int MAXK, int B>
 struct PairSmem {
     static constexpr int W = (MAXK + 63) / 64;  // 64-bit words per mask row
-    static constexpr int CL = 4 * MAXK;         // redirect-capable pairs whose distance is kept
+    static constexpr int CL = 64;  // redirect-capable pairs kept (~0.02% of pairs; overflow re-evaluated)
     uint64_t cond[B][MAXK * W];
     uint64_t afar[B][MAXK * W];
     int32_t ids[2][B][MAXK];  // pool rows of the current / next batch
     float dv[2][B][MAXK];
-    int32_t pos[2][B][MAXK];  // slot -> permutation position
+    uint8_t pos[2][B][MAXK];  // slot -> permutation position
     int32_t k[2][B];
     int64_t v[2][B];          // local row of each batch member (-1: none)
     uint32_t cl_key[B][CL];   // (anchor pos << 8) | partner pos
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(THREADS) pairs_kernel(PropArgs a, int bin, int
                 if (s < nk[r]) {
                     sm.ids[slot][g][s] = nid[r];
                     sm.dv[slot][g][s] = ndv[r];
-                    sm.pos[slot][g][s] = npos[r];
+                    sm.pos[slot][g][s] = (uint8_t)npos[r];
                 }
                 if (s == 0) {
                     sm.k[slot][g] = nk[r];
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(THREADS) pairs_kernel(PropArgs a, int bin, int
                         const int32_t it2 = sm.ids[cur][g][t];
                         r += (dt < ds || (dt == ds && (it2 < is || (it2 == is && t < s)))) ? 1 : 0;
                     }
-                    sm.pos[cur][g][s] = r;
+                    sm.pos[cur][g][s] = (uint8_t)r;
                     a.w.pos8[sm.v[cur][g] * cap + s] = (uint8_t)r;
                 }
             }
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(THREADS) pairs_kernel(PropArgs a, int bin, int
                 gc[e] = wd < W ? sm.cond[g][x * W + wd] : 0ull;
                 ga[e] = wd < W ? sm.afar[g][x * W + wd] : 0ull;
             }
-            const int lcap = 4 * (MAXK < cap ? MAXK : cap);
+            const int lcap = S::CL < 4 * cap ? S::CL : 4 * cap;
             const int ncl = sm.cl_n[g];
             const int nw = ncl < lcap ? ncl : lcap;
             if (tid == 0) a.w.cl_n[v] = nw;  // truncated lists: decide re-evaluates misses

@@ -455,7 +455,10 @@ int launch_propagate(const PropArgs &a, cudaStream_t st) {
     GRNND_TRY(check_launch("bin_kernel"));
     // largest k first so long CTAs start early
     if (a.cap > 128) GRNND_TRY((launch_pairs<256, 1, 256, 3, 4>(a, 5, st)));
-    if (a.cap > 64) GRNND_TRY((launch_pairs<128, 1, 128, 3, 4>(a, 4, st)));
+    // k in (64, 96] with R <= 96 (the benchmark shape): a slab sized for 96 rows fits four
+    // CTAs per SM where the 128-row one fits three
+    if (a.cap > 64 && a.cap <= 96) GRNND_TRY((launch_pairs<96, 1, 128, 3, 4>(a, 4, st)));
+    if (a.cap > 96) GRNND_TRY((launch_pairs<128, 1, 128, 3, 4>(a, 4, st)));
     if (a.cap > 32) GRNND_TRY((launch_pairs<64, 1, 128, 3, 2>(a, 3, st)));
     if (a.cap > 16) GRNND_TRY((launch_pairs<32, GRNND_B2_BATCH, 128, 3, 2>(a, 2, st)));
     if (a.cap > 1) GRNND_TRY((launch_pairs<16, GRNND_B1_BATCH, 128, 2, 2>(a, 1, st)));
