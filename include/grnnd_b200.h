@@ -153,7 +153,17 @@ typedef struct {
     size_t workspace_bytes;
     int64_t msg_capacity; /* messages one round may emit / receive on this rank             */
     int64_t *stats;    /* device int64 [GRNND_NSTATS], accumulated by the round calls      */
+    const float *norms; /* fp32 [n_total] squared row norms (grnnd_row_norms) enabling the
+                           filtered pair phase, or NULL for the exact-only pair phase; the
+                           built graph is the same either way                              */
 } grnnd_pools;
+
+/* Squared L2 norm of every row of data[n, ld] (first dim columns) into out[n] (device).
+ * Feeds grnnd_pools.norms: the pair phase then pre-screens pairs with FFMA dot products
+ * and re-evaluates only the pairs within a rigorous error bound of the redirect
+ * threshold exactly, so every decision and distance stays bit-identical. */
+int grnnd_row_norms(const float *data, int64_t n, int32_t dim, int32_t ld, float *out,
+                    grnnd_stream_t s);
 
 /* builder.init_neighbors (:221-257): sample S ids, their distances, count = S.
  * fail_flag: device int64[1]. */

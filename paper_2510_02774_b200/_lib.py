@@ -53,6 +53,7 @@ class Pools(C.Structure):
         ("workspace_bytes", _sz),
         ("msg_capacity", _i64),
         ("stats", _vp),
+        ("norms", _vp),
     ]
 
 
@@ -91,6 +92,7 @@ _SIGS = {
     "grnnd_sorted_rows": (C.c_int, [_vp, _vp, _vp, _i64, _i32, _vp, _vp]),
     "grnnd_finalize_pools": (C.c_int, [C.POINTER(Pools), _vp, _vp, _vp, _vp]),
     "grnnd_check_finite": (C.c_int, [_vp, _i64, _i32, _i32, _vp, _vp]),
+    "grnnd_row_norms": (C.c_int, [_vp, _i64, _i32, _i32, _vp, _vp]),
 }
 
 if not LIB_PATH.exists():

@@ -19,6 +19,7 @@ raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import warnings
 from dataclasses import dataclass, field, replace
 from typing import Literal, NamedTuple
@@ -179,7 +180,7 @@ class _DevicePools:
     """The double-buffered pools of owned rows [lo, hi) plus round scratch, in HBM."""
 
     def __init__(self, data_dev: torch.Tensor, dim: int, cap: int, lo: int = 0, hi: int | None = None,
-                 n_total: int | None = None, msg_capacity: int | None = None):
+                 n_total: int | None = None, msg_capacity: int | None = None, filtered: bool | None = None):
         dev = data_dev.device
         self.dev = dev
         self.data = data_dev
@@ -204,6 +205,15 @@ class _DevicePools:
         ws = int(_lib.lib.grnnd_workspace_bytes(rows, cap, self.msg_capacity))
         self.workspace = torch.zeros(ws, dtype=torch.uint8, device=dev)
         self.scratch_stats = torch.zeros(_lib.NSTATS, dtype=torch.int64, device=dev)
+        # filtered pair phase (FFMA dot pre-screen + exact re-evaluation near the threshold;
+        # same graph as the exact-only phase): needs the squared norms of every row
+        if filtered is None:
+            filtered = os.environ.get("GRNND_EXACT_PAIRS", "0") != "1"
+        self.norms = None
+        if filtered:
+            self.norms = torch.empty(self.n_total, dtype=f32, device=dev)
+            _lib.call("grnnd_row_norms", data_dev.data_ptr(), self.n_total, self.dim, self.ld,
+                      self.norms.data_ptr(), _stream(dev))
 
     def struct(self, stats: torch.Tensor | None = None) -> _lib.Pools:
         return _lib.Pools(
@@ -212,6 +222,7 @@ class _DevicePools:
             self.write_ids.data_ptr(), self.write_dists.data_ptr(), self.write_count.data_ptr(),
             self.workspace.data_ptr(), self.workspace.numel(), self.msg_capacity,
             (stats if stats is not None else self.scratch_stats).data_ptr(),
+            self.norms.data_ptr() if self.norms is not None else None,
         )
 
     def swap(self) -> None:

@@ -310,6 +310,8 @@ static int emit_update(const grnnd_pools *p, const Workspace &w, uint64_t seed, 
     a.slice_mode = 0;
     a.w = w;
     a.stats = p->stats;
+    a.norms = p->norms;
+    filter_eps(p->dim, &a.eps_n, &a.eps_h);
     return launch_propagate(a, st);
 }
 
@@ -469,6 +471,14 @@ int grnnd_sorted_rows(const int32_t *ids, const float *dists, const int32_t *cou
         return GRNND_EUNSUPPORTED;
     }
     return launch_finalize(ids, dists, counts, n, cap, 0, n, nullptr, nullptr, out_ids, nullptr, S(s));
+}
+
+int grnnd_row_norms(const float *data, int64_t n, int32_t dim, int32_t ld, float *out, grnnd_stream_t s) {
+    if (dim < 1 || ld < dim || n < 0) {
+        set_error("row_norms: bad n/dim/ld");
+        return GRNND_EINVAL;
+    }
+    return launch_row_norms(data, n, dim, ld, out, S(s));
 }
 
 int grnnd_check_finite(const float *data, int64_t n, int32_t dim, int32_t ld, int64_t *bad_flag, grnnd_stream_t s) {

@@ -17,24 +17,50 @@ struct PairSmem {
     int32_t ids[2][B][MAXK];  // pool rows of the current / next batch
     float dv[2][B][MAXK];
     uint8_t pos[2][B][MAXK];  // slot -> permutation position
+    float nrm[2][B][MAXK];    // squared norms of the pool members' rows (filtered mode)
     int32_t k[2][B];
     int64_t v[2][B];          // local row of each batch member (-1: none)
     uint32_t cl_key[B][CL];   // (anchor pos << 8) | partner pos
     float cl_d[B][CL];
     int cl_n[B];
     int tp[B + 1];            // tile prefix over the batch members
+    static constexpr int QC = 256;  // filter candidates per batch (overflow: exact sweep)
+    uint32_t q[QC];           // (member << 16) | (slot s << 8) | slot u
+    int qn;
 };
 
-// redirect condition of the T*T pairs of tile (bI, bJ) of member g, as bits in
-// permutation space, plus the distance of each redirect-capable pair
-template <int MAXK, int B, int T>
-__device__ __forceinline__ unsigned tile_epilogue(PairSmem<MAXK, B> &sm, int cur, int g, const float (&acc)[T * T],
-                                                  int bI, int bJ, int nb, int k) {
+// A redirect-capable pair (s, u) of member g with its exact distance d < max(dv[s], dv[u]):
+// set its bits in permutation space and keep the distance for the decide kernel.
+template <int MAXK, int B>
+__device__ __forceinline__ void record_redirect(PairSmem<MAXK, B> &sm, int cur, int g, int s, int u, float d) {
     using S = PairSmem<MAXK, B>;
     constexpr int W = S::W;
-    // the tile's 2T pool entries once (not per pair); the common "no redirect" outcome is
-    // branch free, only redirect-capable pairs (~0.02% of pairs) take the atomic path
-    float dA[T], dB[T];
+    const int x1 = sm.pos[cur][g][s], x2 = sm.pos[cur][g][u];
+    const float d1 = sm.dv[cur][g][s], d2 = sm.dv[cur][g][u];
+    // anchor = the member visited first (smaller position)
+    const int xa = x1 < x2 ? x1 : x2, xb = x1 < x2 ? x2 : x1;
+    const float dva = x1 < x2 ? d1 : d2, dvb = x1 < x2 ? d2 : d1;
+    const unsigned long long bit = 1ull << (xb & 63);
+    atomicOr((unsigned long long *)&sm.cond[g][xa * W + (xb >> 6)], bit);
+    if (!(dvb >= dva)) atomicOr((unsigned long long *)&sm.afar[g][xa * W + (xb >> 6)], bit);
+    const int c = atomicAdd(&sm.cl_n[g], 1);
+    if (c < S::CL) {
+        sm.cl_key[g][c] = (uint32_t)((xa << 8) | xb);
+        sm.cl_d[g][c] = d;
+    }
+}
+
+// Epilogue of tile (bI, bJ) of member g.
+//  exact (DOT = false): acc holds the reference's sequential distances; decide directly.
+//  filtered (DOT = true): acc holds FFMA dot products; d~ = |a|^2 + |b|^2 - 2 a.b is within
+//  E = eps_n (|a|^2 + |b|^2) + eps_h hi of the exact sequential distance (forward error
+//  bound of both summations, 2x margin), so a pair with d~ >= hi + E can not
+//  redirect and is settled here; the rest (~1% of pairs) are queued for an exact
+//  re-evaluation.  NaN/inf compare false and are queued too.
+template <int MAXK, int B, int T, bool DOT>
+__device__ __forceinline__ unsigned tile_epilogue(PairSmem<MAXK, B> &sm, int cur, int g, const float (&acc)[T * T],
+                                                  int bI, int bJ, int nb, int k, float eps_n, float eps_h) {
+    float dA[T], dB[T], nA[T], nB[T];
     bool vA[T], vB[T];
 #pragma unroll
     for (int i = 0; i < T; ++i) {
@@ -43,6 +69,10 @@ __device__ __forceinline__ unsigned tile_epilogue(PairSmem<MAXK, B> &sm, int cur
         vB[i] = u < k && sm.ids[cur][g][u] != TOMB;
         dA[i] = vA[i] ? sm.dv[cur][g][s] : 0.0f;
         dB[i] = vB[i] ? sm.dv[cur][g][u] : 0.0f;
+        if (DOT) {
+            nA[i] = vA[i] ? sm.nrm[cur][g][s] : 0.0f;
+            nB[i] = vB[i] ? sm.nrm[cur][g][u] : 0.0f;
+        }
     }
     unsigned npairs = 0;
 #pragma unroll
@@ -55,29 +85,39 @@ __device__ __forceinline__ unsigned tile_epilogue(PairSmem<MAXK, B> &sm, int cur
             npairs += valid ? 1u : 0u;
             const float d1 = dA[i], d2 = dB[j];
             const float hi = d1 >= d2 ? d1 : d2;
-            if (valid && acc[i * T + j] < hi) {
-                {
-                    const int x1 = sm.pos[cur][g][s], x2 = sm.pos[cur][g][u];
-                    // anchor = the member visited first (smaller position)
-                    const int xa = x1 < x2 ? x1 : x2, xb = x1 < x2 ? x2 : x1;
-                    const float dva = x1 < x2 ? d1 : d2, dvb = x1 < x2 ? d2 : d1;
-                    const unsigned long long bit = 1ull << (xb & 63);
-                    atomicOr((unsigned long long *)&sm.cond[g][xa * W + (xb >> 6)], bit);
-                    if (!(dvb >= dva)) atomicOr((unsigned long long *)&sm.afar[g][xa * W + (xb >> 6)], bit);
-                    const int c = atomicAdd(&sm.cl_n[g], 1);
-                    if (c < S::CL) {
-                        sm.cl_key[g][c] = (uint32_t)((xa << 8) | xb);
-                        sm.cl_d[g][c] = acc[i * T + j];
-                    }
+            if (DOT) {
+                const float nn = nA[i] + nB[j];
+                const float dap = fmaf(-2.0f, acc[i * T + j], nn);
+                const float e = fmaf(eps_n, nn, fmaf(eps_h, hi, 1e-30f));
+                // settled iff d~ >= hi + E with finite norms; NaN / overflow fall through
+                if (valid && !(dap >= hi + e && nn <= 3.0e38f)) {
+                    const int c = atomicAdd(&sm.qn, 1);
+                    if (c < PairSmem<MAXK, B>::QC) sm.q[c] = (uint32_t)((g << 16) | (s << 8) | u);
                 }
+            } else if (valid && acc[i * T + j] < hi) {
+                record_redirect<MAXK, B>(sm, cur, g, s, u, acc[i * T + j]);
             }
         }
     return npairs;
 }
 
+// Exact sequential distance of two staged rows (the reference's _sqdist arithmetic).
+__device__ __forceinline__ float exact_sqdist_smem(const float4 *__restrict__ a, const float4 *__restrict__ b,
+                                                   int nq) {
+    float s = 0.0f;
+    for (int q = 0; q < nq; ++q) {
+        const float4 x = a[q], y = b[q];
+        s = exact_step(s, x.x, y.x);
+        s = exact_step(s, x.y, y.y);
+        s = exact_step(s, x.z, y.z);
+        s = exact_step(s, x.w, y.w);
+    }
+    return s;
+}
+
 // MULTI: D > 128, rows staged 128 dims at a time with accumulators held across chunks
-// (always B = 1).
-template <int MAXK, int B, int THREADS, int TPT, int T, bool MULTI, int NQ>
+// (always B = 1).  DOT: filtered mode (tile_epilogue); the kernel then needs a.norms.
+template <int MAXK, int B, int THREADS, int TPT, int T, bool MULTI, int NQ, bool DOT>
 __global__ void __launch_bounds__(THREADS) pairs_kernel(PropArgs a, int bin, int kmax) {
     using S = PairSmem<MAXK, B>;
     constexpr int W = S::W;
@@ -95,10 +135,12 @@ __global__ void __launch_bounds__(THREADS) pairs_kernel(PropArgs a, int bin, int
     const int nchunks = (nq_total + DC4 - 1) / DC4;
     const int cap = a.cap;
     const int mw = a.w.mw;
+    const float eps_n = a.eps_n, eps_h = a.eps_h;
     unsigned long long pairs_local = 0;
 
     int32_t nid[PER];
     float ndv[PER];
+    float nnr[PER];
     int32_t npos[PER];
     int nk[PER];
     int64_t nv[PER];
@@ -118,6 +160,7 @@ __global__ void __launch_bounds__(THREADS) pairs_kernel(PropArgs a, int bin, int
                     nid[r] = a.read_ids[v * cap + s];
                     ndv[r] = a.read_dists[v * cap + s];
                     npos[r] = a.order_code == 0 ? (int32_t)a.w.pos8[v * cap + s] : 0;
+                    if (DOT) nnr[r] = nid[r] >= 0 ? a.norms[nid[r]] : 0.0f;
                 }
             }
         }
@@ -132,6 +175,7 @@ __global__ void __launch_bounds__(THREADS) pairs_kernel(PropArgs a, int bin, int
                     sm.ids[slot][g][s] = nid[r];
                     sm.dv[slot][g][s] = ndv[r];
                     sm.pos[slot][g][s] = (uint8_t)npos[r];
+                    if (DOT) sm.nrm[slot][g][s] = nnr[r];
                 }
                 if (s == 0) {
                     sm.k[slot][g] = nk[r];
@@ -207,6 +251,7 @@ __global__ void __launch_bounds__(THREADS) pairs_kernel(PropArgs a, int bin, int
                 t += nb * (nb + 1) / 2;
             }
             sm.tp[B] = t;
+            sm.qn = 0;
         }
         if (has_next) fetch_meta(bi_next);
 
@@ -226,12 +271,10 @@ __global__ void __launch_bounds__(THREADS) pairs_kernel(PropArgs a, int bin, int
                 const int r0 = g * kmax;
                 const int kg = sm.k[cur][g];
                 const int nb = (kg + T - 1) / T;
-                tile_accumulate<T, NQ>(acc, rows, r0 + bI, r0 + bJ, nb, nq_total, rs4);
-                pairs_local += tile_epilogue<MAXK, B, T>(sm, cur, g, acc, bI, bJ, nb, kg);
+                if (DOT) tile_dot<T, NQ>(acc, rows, r0 + bI, r0 + bJ, nb, nq_total, rs4);
+                else tile_accumulate<T, NQ>(acc, rows, r0 + bI, r0 + bJ, nb, nq_total, rs4);
+                pairs_local += tile_epilogue<MAXK, B, T, DOT>(sm, cur, g, acc, bI, bJ, nb, kg, eps_n, eps_h);
             }
-            if (has_next) store_meta(cur ^ 1);
-            __syncthreads();  // masks complete; row slab free; next pool rows visible
-            if (has_next) load_rows(cur ^ 1, 0);  // lands while the masks are written out
         } else {
             const int k = sm.k[cur][0];
             const int nb = (k + T - 1) / T;
@@ -255,7 +298,8 @@ __global__ void __launch_bounds__(THREADS) pairs_kernel(PropArgs a, int bin, int
                         if (t < ntiles) {
                             int bI, bJ;
                             tile_decode(t, bI, bJ);
-                            tile_accumulate<T, 0>(acc[tt], rows, bI, bJ, nb, nq, rs4);
+                            if (DOT) tile_dot<T, 0>(acc[tt], rows, bI, bJ, nb, nq, rs4);
+                            else tile_accumulate<T, 0>(acc[tt], rows, bI, bJ, nb, nq, rs4);
                         }
                     }
                 }
@@ -265,10 +309,52 @@ __global__ void __launch_bounds__(THREADS) pairs_kernel(PropArgs a, int bin, int
                     if (t < ntiles) {
                         int bI, bJ;
                         tile_decode(t, bI, bJ);
-                        pairs_local += tile_epilogue<MAXK, B, T>(sm, cur, 0, acc[tt], bI, bJ, nb, k);
+                        pairs_local += tile_epilogue<MAXK, B, T, DOT>(sm, cur, 0, acc[tt], bI, bJ, nb, k, eps_n, eps_h);
                     }
                 }
             }
+        }
+        if (DOT) {
+            // exact re-evaluation of the filter's candidates (rows still staged unless MULTI)
+            __syncthreads();
+            const int qn = sm.qn;
+            if (qn <= S::QC) {
+                for (int e = tid; e < qn; e += THREADS) {
+                    const uint32_t key = sm.q[e];
+                    const int g = (int)(key >> 16), s = (int)((key >> 8) & 255u), u = (int)(key & 255u);
+                    const float d = MULTI ? exact_sqdist_global(a.data + (int64_t)sm.ids[cur][g][s] * a.ld,
+                                                                a.data + (int64_t)sm.ids[cur][g][u] * a.ld, a.dim)
+                                          : exact_sqdist_smem(rows + (g * kmax + s) * rs4,
+                                                              rows + (g * kmax + u) * rs4, nq_total);
+                    const float d1 = sm.dv[cur][g][s], d2 = sm.dv[cur][g][u];
+                    if (d < (d1 >= d2 ? d1 : d2)) record_redirect<MAXK, B>(sm, cur, g, s, u, d);
+                }
+            } else {
+                // queue overflow (degenerate data: many near-ties): exact sweep of every pair
+#pragma unroll
+                for (int g = 0; g < B; ++g) {
+                    const int k = sm.k[cur][g];
+                    const int np = k * (k - 1) / 2;
+                    for (int p = tid; p < np; p += THREADS) {
+                        int s, u;
+                        tile_decode(p, s, u);  // s <= u over the triangle incl. diagonal
+                        u += 1;                // strict upper triangle: (s, u) with s < u
+                        if (sm.ids[cur][g][s] == TOMB || sm.ids[cur][g][u] == TOMB) continue;
+                        const float d = MULTI ? exact_sqdist_global(a.data + (int64_t)sm.ids[cur][g][s] * a.ld,
+                                                                    a.data + (int64_t)sm.ids[cur][g][u] * a.ld, a.dim)
+                                              : exact_sqdist_smem(rows + (g * kmax + s) * rs4,
+                                                                  rows + (g * kmax + u) * rs4, nq_total);
+                        const float d1 = sm.dv[cur][g][s], d2 = sm.dv[cur][g][u];
+                        if (d < (d1 >= d2 ? d1 : d2)) record_redirect<MAXK, B>(sm, cur, g, s, u, d);
+                    }
+                }
+            }
+        }
+        if (!MULTI) {
+            if (has_next) store_meta(cur ^ 1);
+            __syncthreads();  // masks complete; row slab free; next pool rows visible
+            if (has_next) load_rows(cur ^ 1, 0);  // lands while the masks are written out
+        } else {
             if (has_next) store_meta(cur ^ 1);
             __syncthreads();
         }

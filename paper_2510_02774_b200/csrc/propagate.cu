@@ -166,6 +166,39 @@ __device__ __forceinline__ void tile_accumulate(float (&acc)[T * T], const float
     }
 }
 
+// T*T FFMA dot products (filtered mode): one FP32 op per pair-dim instead of three; the
+// result only pre-screens pairs (tile_epilogue), so its summation order is free
+template <int T, int NQ>
+__device__ __forceinline__ void tile_dot(float (&acc)[T * T], const float4 *__restrict__ rows, int rA, int rB, int nb,
+                                         int nq, int rs4) {
+    const float4 *pa[T], *pb[T];
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+        pa[i] = rows + (rA + nb * i) * rs4;
+        pb[i] = rows + (rB + nb * i) * rs4;
+    }
+    const int n = NQ > 0 ? NQ : nq;
+#pragma unroll 4
+    for (int q = 0; q < n; ++q) {
+        float4 A[T], B[T];
+#pragma unroll
+        for (int i = 0; i < T; ++i) A[i] = pa[i][q];
+#pragma unroll
+        for (int j = 0; j < T; ++j) B[j] = pb[j][q];
+#pragma unroll
+        for (int i = 0; i < T; ++i)
+#pragma unroll
+            for (int j = 0; j < T; ++j) {
+                float s = acc[i * T + j];
+                s = fmaf(A[i].x, B[j].x, s);
+                s = fmaf(A[i].y, B[j].y, s);
+                s = fmaf(A[i].z, B[j].z, s);
+                s = fmaf(A[i].w, B[j].w, s);
+                acc[i * T + j] = s;
+            }
+    }
+}
+
 #include "pairs.cuh"
 
 // ---------------------------------------------------------------------------------
@@ -397,9 +430,6 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) decide_kernel(PropArgs a) {
     }
 }
 
-// ---------------------------------------------------------------------------------
-// host launchers
-// ---------------------------------------------------------------------------------
 static int sm_count() {
     static int s = 0;
     if (!s) {
@@ -411,9 +441,48 @@ static int sm_count() {
     return s;
 }
 
-template <int MAXK, int B, int THREADS, int TPT, int T, bool MULTI, int NQ>
+// ---------------------------------------------------------------------------------
+// squared row norms for the filtered pair phase (warp per row, any summation order:
+// the filter's error bound covers every order)
+// ---------------------------------------------------------------------------------
+__global__ void row_norms_kernel(const float *__restrict__ data, int64_t n, int32_t dim, int32_t ld,
+                                 float *__restrict__ out) {
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int lane = lane_id();
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
+        const float *row = data + r * ld;
+        float s = 0.0f;
+        for (int d = lane; d < dim; d += 32) s = fmaf(row[d], row[d], s);
+        s = warp_sum(s);
+        if (lane == 0) out[r] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------------
+void filter_eps(int32_t dim, float *eps_n, float *eps_h) {
+    // |d~ - d_seq| <= (2 gamma_D + u)(|a|^2 + |b|^2) + (D + 4) u hi near the boundary
+    // (u = 2^-24, gamma_D = D u / (1 - D u)); a 2x margin covers the rounding of the
+    // bound's own evaluation.  DESIGN.md 4 has the derivation.
+    const double u = 1.0 / 16777216.0;
+    const double D = (double)dim;
+    const double g = D * u / (1.0 - D * u);
+    *eps_n = (float)(2.02 * (2.0 * g + u));
+    *eps_h = (float)(2.02 * (D + 5.0) * u);
+}
+
+int launch_row_norms(const float *data, int64_t n, int32_t dim, int32_t ld, float *out, cudaStream_t st) {
+    if (n <= 0) return GRNND_OK;
+    const int64_t blocks = std::min<int64_t>((n + 7) / 8, (int64_t)sm_count() * 32);
+    row_norms_kernel<<<(unsigned)blocks, 256, 0, st>>>(data, n, dim, ld, out);
+    return check_launch("row_norms_kernel");
+}
+
+
+template <int MAXK, int B, int THREADS, int TPT, int T, bool MULTI, int NQ, bool DOT>
 static int launch_pairs_impl(const PropArgs &a, int bin, cudaStream_t st) {
-    auto kern = pairs_kernel<MAXK, B, THREADS, TPT, T, MULTI, NQ>;
+    auto kern = pairs_kernel<MAXK, B, THREADS, TPT, T, MULTI, NQ, DOT>;
     // TxT tiles read rows up to round_up(k, T) - 1: size each member's slab for that
     const int kmax = ((MAXK < a.cap ? MAXK : a.cap) + T - 1) / T * T;
     const int nq_total = (a.dim + 3) >> 2;
@@ -435,12 +504,18 @@ static int launch_pairs_impl(const PropArgs &a, int bin, cudaStream_t st) {
 }
 
 // (MAXK, batch B, threads, tiles/thread kept across 128-dim chunks when D > 128, tile edge T)
+template <int MAXK, int B, int THREADS, int TPT, int T, bool DOT>
+static int launch_pairs_mode(const PropArgs &a, int bin, cudaStream_t st) {
+    const int nq_total = (a.dim + 3) >> 2;
+    if (nq_total == DC4) return launch_pairs_impl<MAXK, B, THREADS, TPT, T, false, DC4, DOT>(a, bin, st);
+    if (a.dim <= DC4 * 4) return launch_pairs_impl<MAXK, B, THREADS, TPT, T, false, 0, DOT>(a, bin, st);
+    return launch_pairs_impl<MAXK, 1, THREADS, TPT, T, true, 0, DOT>(a, bin, st);
+}
+// filtered mode when the caller supplied row norms (the round API), exact mode otherwise
 template <int MAXK, int B, int THREADS, int TPT, int T>
 static int launch_pairs(const PropArgs &a, int bin, cudaStream_t st) {
-    const int nq_total = (a.dim + 3) >> 2;
-    if (nq_total == DC4) return launch_pairs_impl<MAXK, B, THREADS, TPT, T, false, DC4>(a, bin, st);
-    if (a.dim <= DC4 * 4) return launch_pairs_impl<MAXK, B, THREADS, TPT, T, false, 0>(a, bin, st);
-    return launch_pairs_impl<MAXK, 1, THREADS, TPT, T, true, 0>(a, bin, st);
+    if (a.norms) return launch_pairs_mode<MAXK, B, THREADS, TPT, T, true>(a, bin, st);
+    return launch_pairs_mode<MAXK, B, THREADS, TPT, T, false>(a, bin, st);
 }
 
 int launch_propagate(const PropArgs &a, cudaStream_t st) {

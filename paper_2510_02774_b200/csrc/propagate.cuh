@@ -23,7 +23,15 @@ struct PropArgs {
     int32_t *msg_cnt;
     Workspace w;
     int64_t *stats;
+    // filtered pair phase (pairs.cuh): squared row norms of all rows, or nullptr for the
+    // exact-only pair phase; eps_n / eps_h are the filter's error-bound coefficients
+    const float *norms;
+    float eps_n, eps_h;
 };
+
+// error-bound coefficients of the filtered pair phase for dimension dim
+void filter_eps(int32_t dim, float *eps_n, float *eps_h);
+int launch_row_norms(const float *data, int64_t n, int32_t dim, int32_t ld, float *out, cudaStream_t st);
 
 int launch_propagate(const PropArgs &a, cudaStream_t st);
 

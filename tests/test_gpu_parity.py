@@ -305,3 +305,41 @@ def test_recall_parity_acceptance_corpus(g, golden):
     q = generate(100, 16, "uniform", seed=2).data
     ids = oracle.greedy_search(graph.offsets, graph.neighbor_ids, ds.data, q, 64, 10)
     assert oracle.mean_recall(ids, a["truth"]) == pytest.approx(0.9770, abs=1e-12)
+
+
+# ------------------------------------------------------------------ filtered vs exact pair phase
+@pytest.mark.parametrize(
+    "n,dim,dist,S,R,T1,T2,seed",
+    [
+        (20000, 128, "gaussian", 20, 96, 2, 3, 1),
+        (4000, 200, "gaussian", 12, 40, 2, 2, 3),    # D > 128: candidates re-evaluated from global rows
+        (3000, 24, "clustered", 16, 130, 2, 3, 9),
+    ],
+)
+def test_exact_only_pair_phase_bit_exact(g, monkeypatch, n, dim, dist, S, R, T1, T2, seed):
+    """The exact-only pair phase (no norms: every pair in the reference's arithmetic)
+    and the default filtered phase build the same graph as the oracle."""
+    ds = generate(n, dim, dist, seed=seed)
+    params = g.BuildParams(S=S, R=R, T1=T1, T2=T2, rho=0.6, seed=seed)
+    monkeypatch.setenv("GRNND_EXACT_PAIRS", "1")
+    exact = g.build(ds, params)
+    monkeypatch.delenv("GRNND_EXACT_PAIRS")
+    filt = g.build(ds, params)
+    off, nb = oracle.build(ds.data, S, R, T1, T2, 0.6, seed)
+    assert np.array_equal(exact.offsets, off) and np.array_equal(exact.neighbor_ids, nb)
+    assert np.array_equal(filt.offsets, off) and np.array_equal(filt.neighbor_ids, nb)
+
+
+@pytest.mark.parametrize("dim", [16, 128, 160])
+def test_filter_degenerate_ties_and_large_norms(g, dim):
+    """Filter stress: exact duplicates (d = 0 = hi, every pair a candidate: the candidate
+    queue overflows into the exact sweep) and rows far from the origin (|a|^2 >> d, so the
+    error band is wide)."""
+    r = np.random.default_rng(dim)
+    base = r.standard_normal((60, dim)).astype(np.float32)
+    dup = base[r.integers(0, 60, 3000)]
+    far = (r.standard_normal((3000, dim)) * 0.05 + 300.0).astype(np.float32)
+    for x in (dup, far):
+        graph = g.build(g.Dataset(x), g.BuildParams(S=16, R=96, T1=2, T2=3, rho=0.6, seed=4))
+        off, nb = oracle.build(x, 16, 96, 2, 3, 0.6, 4)
+        assert np.array_equal(graph.offsets, off) and np.array_equal(graph.neighbor_ids, nb)
