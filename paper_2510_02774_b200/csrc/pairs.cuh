@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(THREADS) pairs_kernel(PropArgs a, int bin, int
     const int tid = threadIdx.x;
     const int64_t nbin = (int64_t)a.w.ctr[C_BIN0 + bin];
     const int64_t nbatch = (nbin + B - 1) / B;
-    const int32_t *blist = a.w.bins + (int64_t)bin * a.w.n;
+    const int2 *blist = a.w.bins + (int64_t)bin * a.w.n;
     const int nq_total = (a.dim + 3) >> 2;  // float4 per row (ld % 4 == 0, pad cols are 0)
     const int rs4 = row_stride16(nq_total);
     const int nchunks = (nq_total + DC4 - 1) / DC4;
@@ -152,14 +152,15 @@ __global__ void __launch_bounds__(THREADS) pairs_kernel(PropArgs a, int bin, int
             nk[r] = 0;
             nv[r] = -1;
             if (g < B && bi * B + g < nbin) {
-                const int64_t v = blist[bi * B + g];
-                const int k = a.read_count[v];
+                const int2 vk = blist[bi * B + g];
+                const int64_t v = vk.x;
+                const int k = vk.y;
                 nv[r] = v;
                 nk[r] = k;
                 if (s < k) {
                     nid[r] = a.read_ids[v * cap + s];
                     ndv[r] = a.read_dists[v * cap + s];
-                    npos[r] = a.order_code == 0 ? (int32_t)a.w.pos8[v * cap + s] : 0;
+                    npos[r] = a.order_code == 0 ? (int32_t)a.w.pos8[v * a.w.pcap + s] : 0;
                     if (DOT) nnr[r] = nid[r] >= 0 ? a.norms[nid[r]] : 0.0f;
                 }
             }
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(THREADS) pairs_kernel(PropArgs a, int bin, int
                         r += (dt < ds || (dt == ds && (it2 < is || (it2 == is && t < s)))) ? 1 : 0;
                     }
                     sm.pos[cur][g][s] = (uint8_t)r;
-                    a.w.pos8[sm.v[cur][g] * cap + s] = (uint8_t)r;
+                    a.w.pos8[sm.v[cur][g] * a.w.pcap + s] = (uint8_t)r;
                 }
             }
         }

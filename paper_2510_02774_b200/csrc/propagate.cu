@@ -70,7 +70,7 @@ __global__ void bin_kernel(const int32_t *__restrict__ read_count, int64_t n, in
             if (lane_id() == leader) base = atomicAdd(&w.ctr[C_BIN0 + b], (unsigned long long)__popc(peers));
             base = __shfl_sync(peers, base, leader);
             const int rank = __popc(peers & ((1u << lane_id()) - 1));
-            w.bins[(int64_t)b * w.n + (int64_t)base + rank] = (int32_t)v;
+            w.bins[(int64_t)b * w.n + (int64_t)base + rank] = make_int2((int)v, k);
             if (order_code == 0) {
                 // perm = identity; for i = k-1..1: swap(perm[i], perm[hash4(seed,stream,v,i) % (i+1)])
                 uint8_t perm[GRNND_MAX_CAP];
@@ -82,7 +82,7 @@ __global__ void bin_kernel(const int32_t *__restrict__ read_count, int64_t n, in
                     perm[i] = perm[j];
                     perm[j] = t;
                 }
-                uint8_t *pos = w.pos8 + v * cap;
+                uint8_t *pos = w.pos8 + v * w.pcap;
                 for (int x = 0; x < k; ++x) pos[perm[x]] = (uint8_t)x;
             }
         } else if (slice_mode) {
@@ -178,13 +178,23 @@ __device__ __forceinline__ void tile_dot(float (&acc)[T * T], const float4 *__re
         pb[i] = rows + (rB + nb * i) * rs4;
     }
     const int n = NQ > 0 ? NQ : nq;
-#pragma unroll 4
+    // operands of column q+1 are loaded before the FFMAs of column q (register double
+    // buffer): the LDS latency overlaps 4*T*T FFMAs instead of stalling each use
+    float4 A[T], B[T];
+#pragma unroll
+    for (int i = 0; i < T; ++i) {
+        A[i] = pa[i][0];
+        B[i] = pb[i][0];
+    }
+#pragma unroll 2
     for (int q = 0; q < n; ++q) {
-        float4 A[T], B[T];
+        float4 An[T], Bn[T];
+        const int qn = q + 1 < n ? q + 1 : q;
 #pragma unroll
-        for (int i = 0; i < T; ++i) A[i] = pa[i][q];
-#pragma unroll
-        for (int j = 0; j < T; ++j) B[j] = pb[j][q];
+        for (int i = 0; i < T; ++i) {
+            An[i] = pa[i][qn];
+            Bn[i] = pb[i][qn];
+        }
 #pragma unroll
         for (int i = 0; i < T; ++i)
 #pragma unroll
@@ -196,10 +206,16 @@ __device__ __forceinline__ void tile_dot(float (&acc)[T * T], const float4 *__re
                 s = fmaf(A[i].w, B[j].w, s);
                 acc[i * T + j] = s;
             }
+#pragma unroll
+        for (int i = 0; i < T; ++i) {
+            A[i] = An[i];
+            B[i] = Bn[i];
+        }
     }
 }
 
 #include "pairs.cuh"
+#include "pairs5.cuh"
 
 // ---------------------------------------------------------------------------------
 // 3. decide kernel: anchor-serial rule over the masks, emission, tombstones
@@ -248,7 +264,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) decide_kernel(PropArgs a) {
         const int64_t vg = a.lo + v;
         for (int s = lane; s < k; s += 32) {
             ids[s] = a.read_ids[v * cap + s];
-            const uint8_t x = a.w.pos8[v * cap + s];
+            const uint8_t x = a.w.pos8[v * a.w.pcap + s];
             pos[s] = x;
             perm[x] = (int16_t)s;
         }
@@ -518,6 +534,27 @@ static int launch_pairs(const PropArgs &a, int bin, cudaStream_t st) {
     return launch_pairs_mode<MAXK, B, THREADS, TPT, T, false>(a, bin, st);
 }
 
+template <int MAXK, int B, int NW, int T, bool BLOCKED>
+static int launch_pairs5(const PropArgs &a, int bin, cudaStream_t st) {
+    const int nq = (a.dim + 3) >> 2;
+    auto kern = nq == 32 ? pairs5_kernel<MAXK, B, NW, T, BLOCKED, 32> : pairs5_kernel<MAXK, B, NW, T, BLOCKED, 0>;
+    const int kmax = ((MAXK < a.cap ? MAXK : a.cap) + T - 1) / T * T;
+    const size_t smem = align_up(sizeof(P5Smem<MAXK, B>), 128) + (size_t)2 * B * kmax * P5_RS4 * 16;
+    GRNND_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    GRNND_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem));
+    if (per_sm < 1) {
+        set_error("pairs5 bin %d: no CTA fits (smem %zu B)", bin, smem);
+        return GRNND_EUNSUPPORTED;
+    }
+    kern<<<sm_count() * per_sm, NW * 32, smem, st>>>(a, bin, kmax);
+    return check_launch("pairs5_kernel");
+}
+
+#ifndef GRNND_P5
+#define GRNND_P5 0  // pipelined CUDA-core variant: measured slower, kept for A/B
+#endif
+
 int launch_propagate(const PropArgs &a, cudaStream_t st) {
     const int64_t n = a.hi - a.lo;
     if (n <= 0) return GRNND_OK;
@@ -530,6 +567,14 @@ int launch_propagate(const PropArgs &a, cudaStream_t st) {
     GRNND_TRY(check_launch("bin_kernel"));
     // largest k first so long CTAs start early
     if (a.cap > 128) GRNND_TRY((launch_pairs<256, 1, 256, 3, 4>(a, 5, st)));
+    if (GRNND_P5 && a.norms && a.dim <= 128 && a.cap <= 128) {
+        // pipelined filtered pair phase (pairs5.cuh)
+        if (a.cap > 64 && a.cap <= 96) GRNND_TRY((launch_pairs5<96, 1, 4, 4, true>(a, 4, st)));
+        if (a.cap > 96) GRNND_TRY((launch_pairs5<128, 1, 4, 4, true>(a, 4, st)));
+        if (a.cap > 32) GRNND_TRY((launch_pairs5<64, 1, 4, 2, true>(a, 3, st)));
+        if (a.cap > 16) GRNND_TRY((launch_pairs5<32, 2, 4, 2, false>(a, 2, st)));
+        if (a.cap > 1) GRNND_TRY((launch_pairs5<16, 4, 4, 2, false>(a, 1, st)));
+    } else {
     // k in (64, 96] with R <= 96 (the benchmark shape): a slab sized for 96 rows fits four
     // CTAs per SM where the 128-row one fits three
     if (a.cap > 64 && a.cap <= 96) GRNND_TRY((launch_pairs<96, 1, 128, 3, 4>(a, 4, st)));
@@ -537,6 +582,7 @@ int launch_propagate(const PropArgs &a, cudaStream_t st) {
     if (a.cap > 32) GRNND_TRY((launch_pairs<64, 1, 128, 3, 2>(a, 3, st)));
     if (a.cap > 16) GRNND_TRY((launch_pairs<32, GRNND_B2_BATCH, 128, 3, 2>(a, 2, st)));
     if (a.cap > 1) GRNND_TRY((launch_pairs<16, GRNND_B1_BATCH, 128, 2, 2>(a, 1, st)));
+    }
     const int64_t blocks = std::min<int64_t>((n + DEC_WARPS - 1) / DEC_WARPS, (int64_t)sm_count() * 16);
     const unsigned g = (unsigned)std::max<int64_t>(1, blocks);
     switch (a.w.mw) {

@@ -3,6 +3,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cuda_runtime.h>
 
 namespace grnnd {
 
@@ -37,9 +38,10 @@ struct Workspace {
     int32_t *in_count;   // [n+1] per-target counts (self-resetting)
     int64_t *starts;     // [n+1]
     int64_t *scan_tmp;   // [scan blocks + 1]
-    int32_t *bins;       // [n] vertex lists, bin b at bins + bin_off[b] ... (packed by counts)
+    int2 *bins;          // [NBINS, n] (vertex row, k) lists per propagate bin
     int32_t *heavy;      // [n] heavy segment ids
-    uint8_t *pos8;       // [n, cap] permutation position of each pool slot (this round)
+    uint8_t *pos8;       // [n, pcap] permutation position of each pool slot (this round)
+    int32_t pcap;        // pos8 row stride = round_up(cap, 4) (4-byte cp.async rows)
     int32_t cap;
     int32_t mw;          // 64-bit words per mask row = ceil(cap / 64)
     uint64_t *cond;      // [n, cap, mw] redirect-condition bits, row = anchor position
@@ -84,9 +86,10 @@ inline size_t carve(Workspace *w, void *base, int64_t n, int32_t cap, int64_t ms
     t.in_count = (int32_t *)take(4 * (N + 1));
     t.starts = (int64_t *)take(8 * (N + 1));
     t.scan_tmp = (int64_t *)take(8 * (size_t)(scan_blocks((int64_t)N) + 2 + 128));
-    t.bins = (int32_t *)take(4 * N * NBINS);
+    t.bins = (int2 *)take(8 * N * NBINS);
     t.heavy = (int32_t *)take(4 * N);
-    t.pos8 = (uint8_t *)take(N * (size_t)(cap > 0 ? cap : 1));
+    t.pcap = (cap > 0 ? cap + 3 : 4) / 4 * 4;
+    t.pos8 = (uint8_t *)take(N * (size_t)t.pcap);
     t.cap = cap;
     t.mw = (cap + 63) / 64 > 0 ? (cap + 63) / 64 : 1;
     t.cond = (uint64_t *)take(8 * N * (size_t)(cap > 0 ? cap : 1) * (size_t)t.mw);
