@@ -57,6 +57,9 @@ enum {
     GRNND_ST_REJECTED = 7,
     GRNND_ST_PAIRS = 8,     /* pair distances computed (all live pairs; instrumentation) */
     GRNND_ST_PAIRS_REF = 9, /* pairs the reference loop would evaluate (instrumentation) */
+    GRNND_ST_CANDIDATES = 10, /* pairs the filtered pair phase re-evaluated exactly (instrumentation) */
+    GRNND_ST_OVERFLOWS = 11,  /* groups whose candidate queue overflowed into an exact sweep */
+    GRNND_ST_REDIRECTABLE = 12, /* pairs meeting the redirect condition (instrumentation)      */
     GRNND_NSTATS = 16
 };
 

@@ -21,7 +21,7 @@ OK, EINVAL, ECUDA, EUNSUPPORTED, EWORKSPACE = 0, 1, 2, 3, 4
 NSTATS = 16
 ST_MESSAGES, ST_REDIRECTS, ST_SURVIVORS, ST_REVERSE_ATTEMPTS = 0, 1, 2, 3
 ST_INSERTED, ST_DUPLICATE, ST_REPLACED, ST_REJECTED = 4, 5, 6, 7
-ST_PAIRS, ST_PAIRS_REF = 8, 9
+ST_PAIRS, ST_PAIRS_REF, ST_CANDIDATES, ST_OVERFLOWS = 8, 9, 10, 11
 MAX_CAP = 256
 
 _vp = C.c_void_p

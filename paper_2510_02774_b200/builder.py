@@ -87,6 +87,7 @@ class RoundStats:
     # instrumentation (not in the reference): pair distances computed / evaluated
     pairs: int = field(default=0, compare=False, repr=False)
     pairs_ref: int = field(default=0, compare=False, repr=False)
+    candidates: int = field(default=0, compare=False, repr=False)  # filter band re-evaluations
 
     @classmethod
     def from_counters(cls, kind: str, c) -> "RoundStats":
@@ -103,6 +104,7 @@ class RoundStats:
             rejected=c[_lib.ST_REJECTED],
             pairs=c[_lib.ST_PAIRS],
             pairs_ref=c[_lib.ST_PAIRS_REF],
+            candidates=c[_lib.ST_CANDIDATES],
         )
         if kind == "update":
             st.survivors = st.messages - st.redirects
@@ -176,6 +178,9 @@ def check_finite_device(data_dev: torch.Tensor, dim: int) -> None:
         raise ParamError("dataset contains non-finite values")
 
 
+EXACT_FIRST_ROUNDS = 3  # update rounds (stream ids 1..3) that run the exact-only pair phase
+
+
 class _DevicePools:
     """The double-buffered pools of owned rows [lo, hi) plus round scratch, in HBM."""
 
@@ -215,15 +220,24 @@ class _DevicePools:
             _lib.call("grnnd_row_norms", data_dev.data_ptr(), self.n_total, self.dim, self.ld,
                       self.norms.data_ptr(), _stream(dev))
 
-    def struct(self, stats: torch.Tensor | None = None) -> _lib.Pools:
+    def struct(self, stats: torch.Tensor | None = None, filtered: bool = True) -> _lib.Pools:
+        norms = self.norms if filtered else None
         return _lib.Pools(
             self.data.data_ptr(), self.n_total, self.lo, self.hi, self.dim, self.ld, self.cap,
             self.read_ids.data_ptr(), self.read_dists.data_ptr(), self.read_count.data_ptr(),
             self.write_ids.data_ptr(), self.write_dists.data_ptr(), self.write_count.data_ptr(),
             self.workspace.data_ptr(), self.workspace.numel(), self.msg_capacity,
             (stats if stats is not None else self.scratch_stats).data_ptr(),
-            self.norms.data_ptr() if self.norms is not None else None,
+            norms.data_ptr() if norms is not None else None,
         )
+
+    @staticmethod
+    def filtered_round(stream_id: int) -> bool:
+        """Pair-phase mode of an update round.  The first rounds start from random pools,
+        where most pairs meet the redirect condition (68% / 32% / 17% of all pairs in rounds
+        1-3 at C2) and the tensor-core filter settles few of them: those rounds run the
+        exact-only pair phase; later rounds the filtered one.  Same graph either way."""
+        return stream_id > int(os.environ.get("GRNND_EXACT_FIRST_ROUNDS", EXACT_FIRST_ROUNDS))
 
     def swap(self) -> None:
         """clear_and_swap (builder.py:170-176): the written buffers become the read
@@ -242,7 +256,7 @@ class _DevicePools:
         return fail
 
     def update(self, seed: int, stream_id: int, order_code: int, stats: torch.Tensor) -> None:
-        p = self.struct(stats)
+        p = self.struct(stats, self.filtered_round(stream_id))
         _lib.call("grnnd_update_round", C.byref(p), seed & MASK64, stream_id & MASK64, order_code,
                   _stream(self.dev))
         self.swap()
@@ -256,7 +270,7 @@ class _DevicePools:
                      ev: tuple | None = None) -> None:
         """update() as its two halves with optional CUDA events (before emit, after emit,
         after apply) for per-phase timing on the launching stream."""
-        p = self.struct(stats)
+        p = self.struct(stats, self.filtered_round(stream_id))
         st = _stream(self.dev)
         if ev:
             ev[0].record()

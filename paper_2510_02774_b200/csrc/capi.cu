@@ -156,6 +156,7 @@ int grnnd_gen_update_messages(const float *data, int64_t n, int32_t dim, int32_t
     GRNND_TRY(check_ws(workspace, workspace_bytes, n, cap, 0, &w));
     PropArgs a{};
     a.data = data;
+    a.n_total = n;
     a.lo = 0;
     a.hi = n;
     a.dim = dim;
@@ -296,6 +297,7 @@ static int emit_update(const grnnd_pools *p, const Workspace &w, uint64_t seed, 
                        int32_t order_code, cudaStream_t st) {
     PropArgs a{};
     a.data = p->data;
+    a.n_total = p->n_total;
     a.lo = p->lo;
     a.hi = p->hi;
     a.dim = p->dim;
@@ -472,6 +474,7 @@ int grnnd_sorted_rows(const int32_t *ids, const float *dists, const int32_t *cou
     }
     return launch_finalize(ids, dists, counts, n, cap, 0, n, nullptr, nullptr, out_ids, nullptr, S(s));
 }
+
 
 int grnnd_row_norms(const float *data, int64_t n, int32_t dim, int32_t ld, float *out, grnnd_stream_t s) {
     if (dim < 1 || ld < dim || n < 0) {

@@ -28,7 +28,9 @@
 
 namespace grnnd {
 
-__device__ __forceinline__ int bin_of(int k) {
+__device__ __forceinline__ int bin_of(int k, int tc_bins) {
+    if (tc_bins)  // tensor-core groups of 96 rows: slot sizes 16, 24, 32, 48, 96 (tc3_pairs.cuh)
+        return k <= 1 ? 0 : k <= 16 ? 1 : k <= 24 ? 2 : k <= 32 ? 3 : k <= 48 ? 4 : 5;
     return k <= 1 ? 0 : k <= 16 ? 1 : k <= 32 ? 2 : k <= 64 ? 3 : k <= 128 ? 4 : 5;
 }
 
@@ -54,7 +56,7 @@ __global__ void bin_kernel(const int32_t *__restrict__ read_count, int64_t n, in
                            int64_t *__restrict__ stats, int slice_mode, const int32_t *__restrict__ read_ids,
                            const float *__restrict__ read_dists, int64_t lo, uint64_t seed, uint64_t stream_id,
                            int order_code, int32_t *__restrict__ msg_tgt, int32_t *__restrict__ msg_id,
-                           float *__restrict__ msg_dist, int32_t *__restrict__ msg_cnt) {
+                           float *__restrict__ msg_dist, int32_t *__restrict__ msg_cnt, int tc_bins) {
     __shared__ unsigned long long s_sum;
     if (threadIdx.x == 0) s_sum = 0;
     __syncthreads();
@@ -62,7 +64,7 @@ __global__ void bin_kernel(const int32_t *__restrict__ read_count, int64_t n, in
     int k = 0;
     if (v < n) {
         k = read_count[v];
-        const int b = bin_of(k);
+        const int b = bin_of(k, tc_bins);
         if (b > 0) {
             const unsigned peers = __match_any_sync(__activemask(), b);
             const int leader = __ffs(peers) - 1;
@@ -216,6 +218,8 @@ __device__ __forceinline__ void tile_dot(float (&acc)[T * T], const float4 *__re
 
 #include "pairs.cuh"
 #include "pairs5.cuh"
+#include "tc_pairs.cuh"
+#include "tc3_pairs.cuh"
 
 // ---------------------------------------------------------------------------------
 // 3. decide kernel: anchor-serial rule over the masks, emission, tombstones
@@ -551,6 +555,36 @@ static int launch_pairs5(const PropArgs &a, int bin, cudaStream_t st) {
     return check_launch("pairs5_kernel");
 }
 
+template <int SZ>
+static int launch_tc_pairs(const PropArgs &a, int bin, cudaStream_t st) {
+    auto kern = tc_pairs_kernel<SZ>;
+    const size_t smem = (size_t)TC_NSTAGE * TC_STAGE_BYTES + sizeof(TcSmem<SZ>) + 1024;
+    static bool configured = false;
+    if (!configured) {
+        GRNND_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = true;
+    }
+    kern<<<sm_count(), TC_THREADS, smem, st>>>(a, bin);
+    return check_launch("tc_pairs_kernel");
+}
+
+template <int SZ>
+static int launch_tc3_pairs(const PropArgs &a, int bin, cudaStream_t st) {
+    auto kern = tc3_pairs_kernel<SZ>;
+    const size_t smem = (size_t)T3_NS * T3_STAGE + T3_PAD + sizeof(T3Smem<SZ>) + 1024;
+    static bool configured = false;
+    if (!configured) {
+        GRNND_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = true;
+    }
+    kern<<<sm_count(), T3_NT, smem, st>>>(a, bin);
+    return check_launch("tc3_pairs_kernel");
+}
+
+#ifndef GRNND_TC
+#define GRNND_TC 1  // tensor-core Gram pre-screen (tc_pairs.cuh) for D <= 128, R <= 128
+#endif
+
 #ifndef GRNND_P5
 #define GRNND_P5 0  // pipelined CUDA-core variant: measured slower, kept for A/B
 #endif
@@ -559,15 +593,29 @@ int launch_propagate(const PropArgs &a, cudaStream_t st) {
     const int64_t n = a.hi - a.lo;
     if (n <= 0) return GRNND_OK;
     GRNND_CUDA(cudaMemsetAsync(a.w.ctr + C_BIN0, 0, sizeof(unsigned long long) * NBINS, st));
+    const bool tc3 = GRNND_TC && a.norms && a.dim <= 128 && a.cap <= T3_ROWS && a.order_code == 0;
     const int tb = 128;
     bin_kernel<<<(unsigned)((n + tb - 1) / tb), tb, 0, st>>>(a.read_count, n, a.cap, a.w, a.stats, a.slice_mode,
                                                             a.read_ids, a.read_dists, a.lo, a.seed, a.stream_id,
                                                             a.order_code, a.msg_tgt, a.msg_id, a.msg_dist,
-                                                            a.msg_cnt);
+                                                            a.msg_cnt, tc3 ? 1 : 0);
     GRNND_TRY(check_launch("bin_kernel"));
     // largest k first so long CTAs start early
     if (a.cap > 128) GRNND_TRY((launch_pairs<256, 1, 256, 3, 4>(a, 5, st)));
-    if (GRNND_P5 && a.norms && a.dim <= 128 && a.cap <= 128) {
+    if (tc3) {
+        tc_stage_kernel<<<sm_count() * 8, 256, 0, st>>>(a);
+        GRNND_TRY(check_launch("tc_stage_kernel"));
+        if (a.cap > 48) GRNND_TRY(launch_tc3_pairs<96>(a, 5, st));
+        if (a.cap > 32) GRNND_TRY(launch_tc3_pairs<48>(a, 4, st));
+        if (a.cap > 24) GRNND_TRY(launch_tc3_pairs<32>(a, 3, st));
+        if (a.cap > 16) GRNND_TRY(launch_tc3_pairs<24>(a, 2, st));
+        if (a.cap > 1) GRNND_TRY(launch_tc3_pairs<16>(a, 1, st));
+    } else if (GRNND_TC && a.norms && a.dim <= 128 && a.cap <= 128 && a.order_code == 0) {
+        if (a.cap > 64) GRNND_TRY(launch_tc_pairs<128>(a, 4, st));
+        if (a.cap > 32) GRNND_TRY(launch_tc_pairs<64>(a, 3, st));
+        if (a.cap > 16) GRNND_TRY(launch_tc_pairs<32>(a, 2, st));
+        if (a.cap > 1) GRNND_TRY(launch_tc_pairs<16>(a, 1, st));
+    } else if (GRNND_P5 && a.norms && a.dim <= 128 && a.cap <= 128) {
         // pipelined filtered pair phase (pairs5.cuh)
         if (a.cap > 64 && a.cap <= 96) GRNND_TRY((launch_pairs5<96, 1, 4, 4, true>(a, 4, st)));
         if (a.cap > 96) GRNND_TRY((launch_pairs5<128, 1, 4, 4, true>(a, 4, st)));
@@ -596,3 +644,19 @@ int launch_propagate(const PropArgs &a, cudaStream_t st) {
 }
 
 }  // namespace grnnd
+
+#ifdef GRNND_T3_PROF
+// profiling builds only: role timers of tc3_pairs_kernel (read and reset)
+extern "C" int grnnd_debug_counters(unsigned long long *out, int n) {
+    unsigned long long buf[32] = {0};
+    if (cudaMemcpyFromSymbol(buf, grnnd::g_t3prof, sizeof(buf)) != cudaSuccess) return GRNND_ECUDA;
+    for (int i = 0; i < n && i < 32; ++i) out[i] = buf[i];
+    unsigned long long z[32] = {0};
+    if (cudaMemcpyToSymbol(grnnd::g_t3prof, z, sizeof(z)) != cudaSuccess) return GRNND_ECUDA;
+    return GRNND_OK;
+}
+extern "C" int grnnd_debug_trace(long long *out) {  // 64 x 8 event clocks of CTA 0
+    if (cudaMemcpyFromSymbol(out, grnnd::g_t3trace, sizeof(long long) * 512) != cudaSuccess) return GRNND_ECUDA;
+    return GRNND_OK;
+}
+#endif

@@ -9,6 +9,7 @@ namespace grnnd {
 
 struct PropArgs {
     const float *data;
+    int64_t n_total;  // rows of data (the TMA tensor map's extent)
     int64_t lo, hi;  // owned rows [lo, hi) ; row r of the pool arrays = vertex lo + r
     int32_t dim, ld, cap;
     int32_t *read_ids;

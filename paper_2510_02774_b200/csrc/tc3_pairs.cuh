@@ -1,0 +1,493 @@
+// tc3_pairs.cuh -- warp-specialised tensor-core pair phase for D <= 128, R <= 96 (the
+// benchmark shape).  Included by propagate.cu inside namespace grnnd after tc_pairs.cuh.
+//
+// Same contract and filter as tc_pairs.cuh: the Gram of a group of pool rows on
+// tcgen05.mma.kind::tf32, a rigorous error band around the redirect threshold, and the
+// reference's exact sequential fp32 arithmetic for the pairs inside the band -- so every
+// decision and emitted distance is bit-identical to the reference.  The schedule has no
+// CTA-wide barrier per group and no dependent global load on its critical path:
+//   * tc_stage_kernel (propagate.cu) lays every group's metadata out contiguously (pool
+//     ids, stored distances, permutation positions, row norms, (vertex, k) header);
+//   warp 0       metadata: one thread streams group g's metadata into meta slot g % 8 with
+//                1-D bulk copies (TMA), completing on mfull[m];
+//   warps 8-19   row producers: cp.async of the 96 vector rows into stage g % 4 (K-major,
+//                128-byte swizzle); completion arrives on full[s] in hardware
+//                (cp.async.mbarrier.arrive.noinc).  Random 512-byte row gathers need ~16
+//                issuing warps per SM to approach HBM bandwidth (a warp's cp.async stream is
+//                capped near 4-5 GB/s, TMA boxes near 1-3.6 TB/s chip-wide for this access
+//                size: tools/ubench_gather*.cu);
+//   warp 1       MMA: one thread fences the async proxy and issues the 16 MMAs of group g
+//                into TMEM accumulator g % 2;
+//   warps 4-6    filter (TMEM lanes 0..95): Gram -> band candidates -> queue g % 2;
+//   warps 2,3,7  exact chains of the queue -> redirect masks -> global; release the stage
+//                and the meta slot.
+// Groups: 96 rows = one pool of k <= 96, or 96/SZ pools of k <= SZ (SZ = 16, 24, 32, 48).
+#pragma once
+
+constexpr int T3_ROWS = 96;
+constexpr int T3_KB = T3_ROWS * 128;  // one 32-dim k-block of a stage (12 KB)
+constexpr int T3_STAGE = 4 * T3_KB;   // 96 rows x 128 fp32 (48 KB)
+constexpr int T3_NS = 4;              // row stages
+constexpr int T3_NM = 8;              // metadata slots
+constexpr int T3_PAD = 4096;          // the M = 128 MMA reads 32 rows past the last k-block
+constexpr int T3_NT = 640;            // 20 warps
+constexpr int T3_NP = 12;             // row-producer warps (8..19)
+
+struct T3Meta {  // one group's metadata, filled by bulk copies from the staging arrays
+    int32_t ids[T3_ROWS];
+    float dv[T3_ROWS];
+    float nrm[T3_ROWS];
+    uint8_t pos[T3_ROWS];
+    int2 hdr[8];  // (vertex row, k) of pool p < GP
+};
+constexpr uint32_t T3_META_BYTES = 3 * 4 * T3_ROWS + T3_ROWS + 64;
+
+template <int SZ>
+struct T3Smem {
+    static constexpr int GP = T3_ROWS / SZ;
+    static constexpr int CL = 64;    // kept redirect distances per pool
+    static constexpr int QC = 1024;  // filter candidates per group (overflow: exact sweep)
+    T3Meta meta[T3_NM];
+    float2 ab[2][T3_ROWS];        // filter terms (A = -inf: always a candidate; B = -1: dead row)
+    uint64_t cond[T3_ROWS][2];    // row = p * SZ + anchor position; bit = partner position
+    uint64_t afar[T3_ROWS][2];
+    uint32_t cl_key[GP][CL];
+    float cl_d[GP][CL];
+    int cl_n[2][GP];
+    int qn[2];
+    uint32_t q[2][QC];            // (row i << 8) | row j
+    uint64_t mfull[T3_NM], mempty[T3_NM], full[T3_NS], empty[T3_NS], accf[2], acce[2], qrdy[2], qemp[2];
+    uint32_t tmem_base;
+};
+
+namespace tc {
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+}  // namespace tc
+
+__device__ __forceinline__ uint32_t t3_off(int r, int c) {
+    return (uint32_t)((c >> 3) * T3_KB + (r >> 3) * 1024 + (r & 7) * 128 + (((c & 7) ^ (r & 7)) << 4));
+}
+
+// TC bins 1..5 (slot sizes 16, 24, 32, 48, 96): groups of bin b start at staging group
+// tc_group_base(b) (all bins' groups back to back)
+__host__ __device__ __forceinline__ int tc_bin_gp(int b) { return b == 1 ? 6 : b == 2 ? 4 : b == 3 ? 3 : b == 4 ? 2 : 1; }
+__host__ __device__ __forceinline__ int tc_bin_sz(int b) { return 96 / tc_bin_gp(b); }
+__device__ __forceinline__ int64_t tc_group_base(const unsigned long long *ctr, int b) {
+    int64_t base = 0;
+    for (int x = 1; x < b; ++x) {
+        const int gp = tc_bin_gp(x);
+        base += ((int64_t)ctr[C_BIN0 + x] + gp - 1) / gp;
+    }
+    return base;
+}
+
+#ifdef GRNND_T3_PROF
+__device__ unsigned long long g_t3prof[32];
+__device__ long long g_t3trace[64][8];  // CTA 0: per group event times (profiling builds)
+#define T3P_BEGIN() const long long _t3p0 = clock64()
+#define T3P_ADD(slot, since) atomicAdd(&g_t3prof[slot], (unsigned long long)(clock64() - (since)))
+#define T3P_EV(g, ev) do { if (blockIdx.x == 0 && (g) < 64) g_t3trace[(g)][(ev)] = clock64(); } while (0)
+#define T3P_WAIT(slot, stmt) do { const long long _w = clock64(); stmt; if (lane == 0) T3P_ADD(slot, _w); } while (0)
+#else
+#define T3P_BEGIN()
+#define T3P_ADD(slot, since)
+#define T3P_EV(g, ev)
+#define T3P_WAIT(slot, stmt) stmt
+#endif
+
+template <int SZ>
+__global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin) {
+    using S = T3Smem<SZ>;
+    constexpr int GP = S::GP;
+    constexpr int R = T3_ROWS;
+    constexpr int NS = T3_NS;
+    constexpr int NM = T3_NM;
+    extern __shared__ __align__(1024) unsigned char t3_raw[];
+    unsigned char *base = t3_raw + ((1024 - (tc::smem_u32(t3_raw) & 1023)) & 1023);
+    S &sm = *reinterpret_cast<S *>(base + NS * T3_STAGE + T3_PAD);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t nbin = (int64_t)a.w.ctr[C_BIN0 + bin];
+    const int64_t ngroups = (nbin + GP - 1) / GP;
+    const int64_t G = gridDim.x;
+    if ((int64_t)blockIdx.x >= ngroups) return;
+    const int64_t nmine = (ngroups - blockIdx.x + G - 1) / G;
+    const int64_t gbase = tc_group_base(a.w.ctr, bin);
+    const int nq = (a.dim + 3) >> 2;
+    const int cap = a.cap, mw = a.w.mw;
+    unsigned long long st_pairs = 0, st_cand = 0, st_ovf = 0, st_red = 0;
+
+    // ---- setup ----
+    if (warp == 1) tc::tmem_alloc(&sm.tmem_base, TC_TMEM_COLS);
+    if (tid == 0) {
+        for (int m = 0; m < NM; ++m) {
+            tc::mbar_init(&sm.mfull[m], 1);
+            tc::mbar_init(&sm.mempty[m], 96);
+        }
+        for (int s = 0; s < NS; ++s) {
+            tc::mbar_init(&sm.full[s], T3_NP * 32);
+            tc::mbar_init(&sm.empty[s], 96);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&sm.accf[b], 1);
+            tc::mbar_init(&sm.acce[b], 96);
+            tc::mbar_init(&sm.qrdy[b], 96);
+            tc::mbar_init(&sm.qemp[b], 96);
+        }
+        tc::fence_mbar_init();
+    }
+    for (int i = tid; i < R * 2; i += T3_NT) {
+        (&sm.cond[0][0])[i] = 0ull;
+        (&sm.afar[0][0])[i] = 0ull;
+    }
+    if (tid < 2) sm.qn[tid] = 0;
+    if (tid < 2 * GP) (&sm.cl_n[0][0])[tid] = 0;
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = sm.tmem_base;
+
+    T3P_BEGIN();
+    if (warp == 0) {
+        // ================= metadata (bulk copies of the staged group) =================
+        if (lane == 0) {
+            for (int64_t g = 0; g < nmine; ++g) {
+                const int m = (int)(g % NM);
+                T3P_WAIT(0, tc::mbar_wait(&sm.mempty[m], (uint32_t)(((g / NM) & 1) ^ 1)));
+                const int64_t e0 = (gbase + blockIdx.x + g * G) * R;  // first staging slot of the group
+                T3Meta &mt = sm.meta[m];
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(&sm.mfull[m])),
+                             "r"(T3_META_BYTES)
+                             : "memory");
+                tc::bulk_g2s(mt.ids, a.w.s_ids + e0, 4 * R, &sm.mfull[m]);
+                tc::bulk_g2s(mt.dv, a.w.s_dv + e0, 4 * R, &sm.mfull[m]);
+                tc::bulk_g2s(mt.nrm, a.w.s_nrm + e0, 4 * R, &sm.mfull[m]);
+                tc::bulk_g2s(mt.pos, a.w.s_pos + e0, R, &sm.mfull[m]);
+                tc::bulk_g2s(mt.hdr, a.w.s_hdr + (e0 / R) * 8, 64, &sm.mfull[m]);
+                T3P_EV(g, 0);
+            }
+        }
+        __syncwarp();
+    } else if (warp >= 8) {
+        // ================= row producers (12 warps) =================
+        // warp pi stages group rows pi, pi + 12, ..: one 512-byte row per instruction (lane =
+        // 16-byte chunk, 128-byte swizzle)
+        const int pi = warp - 8;
+        const bool cv = lane < nq;
+        const uint32_t lo = (uint32_t)((lane >> 3) * T3_KB), lx = (uint32_t)(lane & 7);
+        for (int64_t g = 0; g < nmine; ++g) {
+            const int s = (int)(g % NS), m = (int)(g % NM);
+            T3P_WAIT(15, tc::mbar_wait(&sm.mfull[m], (uint32_t)((g / NM) & 1)));
+            T3P_WAIT(16, tc::mbar_wait(&sm.empty[s], (uint32_t)(((g / NS) & 1) ^ 1)));
+            const uint32_t stg = tc::smem_u32(base + s * T3_STAGE);
+#pragma unroll
+            for (int q = 0; q < R / T3_NP; ++q) {
+                const int r = pi + T3_NP * q;
+                const int32_t id = sm.meta[m].ids[r];
+                if (id == TOMB) continue;  // empty slot (warp-uniform)
+                const float *src = a.data + (int64_t)id * a.ld + (cv ? lane * 4 : 0);
+                const uint32_t dst = stg + lo + (uint32_t)((r >> 3) * 1024 + (r & 7) * 128) + ((lx ^ (uint32_t)(r & 7)) << 4);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(cv ? 16 : 0));
+            }
+            if (pi == 0 && lane == 0) T3P_EV(g, 1);
+            // one arrive per lane, performed by the hardware when the lane's copies have landed;
+            // the MMA thread fences the async proxy before the tensor core reads the stage
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&sm.full[s])) : "memory");
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer =================
+        if (lane == 0) {
+            for (int64_t g = 0; g < nmine; ++g) {
+                const int s = (int)(g % NS), m = (int)(g % NM), ac = (int)(g & 1);
+                T3P_WAIT(2, tc::mbar_wait(&sm.full[s], (uint32_t)((g / NS) & 1)));
+                tc::mbar_wait(&sm.mfull[m], (uint32_t)((g / NM) & 1));
+                T3P_WAIT(3, tc::mbar_wait(&sm.acce[ac], (uint32_t)(((g >> 1) & 1) ^ 1)));
+                tc::fence_after();
+                tc::fence_proxy_async();  // cp.async (generic proxy) writes -> tensor core reads
+                const int n = GP == 1 ? ((sm.meta[m].hdr[0].y + 15) / 16 * 16) : R;
+                const uint32_t idesc = tc::idesc_tf32(n < 16 ? 16 : n);
+                const uint32_t sa = tc::smem_u32(base + s * T3_STAGE);
+                const uint32_t d = tmem + (uint32_t)(ac * 128);
+#pragma unroll
+                for (int kb = 0; kb < 4; ++kb)
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint64_t desc = tc::sw128_desc(sa + kb * T3_KB + kk * 32);
+                        tc::mma_tf32(d, desc, desc, idesc, (kb | kk) != 0);
+                    }
+                T3P_EV(g, 3);
+                tc::mma_commit(&sm.accf[ac]);
+            }
+        }
+        __syncwarp();
+    } else if (warp >= 4 && warp <= 6) {
+        // ================= filter (TMEM lanes 0..95) =================
+        const int fw = warp - 4, i = fw * 32 + lane;
+        const float eps_h = a.eps_h + 4.8e-7f;
+        for (int64_t g = 0; g < nmine; ++g) {
+            const int m = (int)(g % NM), b = (int)(g & 1);
+            T3P_WAIT(4, tc::mbar_wait(&sm.mfull[m], (uint32_t)((g / NM) & 1)));
+            const T3Meta &mt = sm.meta[m];
+            {  // this row's filter terms
+                const int p = i / SZ, sl = i - p * SZ;
+                const bool live = sl < mt.hdr[p].y && mt.ids[i] != TOMB;
+                const float nr = mt.nrm[i];
+                float A = nr * (1.0f - TC_EPS);
+                if (!(nr <= 1.0e37f)) A = -INFINITY;  // rearranged test could overflow: always a candidate
+                sm.ab[b][i] = live ? make_float2(A, fmaf(mt.dv[i], 1.0f + eps_h, 1e-30f)) : make_float2(0.0f, -1.0f);
+            }
+            T3P_WAIT(5, tc::named_bar(1, 96));
+            T3P_WAIT(6, tc::mbar_wait(&sm.qemp[b], (uint32_t)(((g >> 1) & 1) ^ 1)));
+            T3P_WAIT(7, tc::mbar_wait(&sm.accf[b], (uint32_t)((g >> 1) & 1)));
+            if (tid == 128) T3P_EV(g, 4);
+            tc::fence_after();
+            const float2 abi = sm.ab[b][i];
+            const int kcols = GP == 1 ? mt.hdr[0].y : R;
+            const uint32_t trow = tmem + ((uint32_t)(fw * 32) << 16) + (uint32_t)(b * 128);
+            unsigned np = 0;
+            // 16 Gram columns [cb, cb+16) of this warp's rows; tr: the columns are the smaller
+            // member of each pair (a block below the diagonal read in place of its transpose)
+            auto scan16 = [&](int cb, bool tr) {
+                uint32_t r[16];
+                tc::tmem_ld16(trow + (uint32_t)cb, r);
+                float4 ab4[8];  // column terms, two columns per 16-byte load
+#pragma unroll
+                for (int c = 0; c < 8; ++c) ab4[c] = *reinterpret_cast<const float4 *>(&sm.ab[b][cb + 2 * c]);
+                uint32_t cm = 0u;
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    const int jr = cb + c;
+                    const float ax = (c & 1) ? ab4[c >> 1].z : ab4[c >> 1].x;
+                    const float ay = (c & 1) ? ab4[c >> 1].w : ab4[c >> 1].y;
+                    const bool valid = (tr ? jr < i : jr > i) && (GP == 1 || (jr / SZ) == (i / SZ)) && ay >= 0.0f &&
+                                       abi.y >= 0.0f;
+                    np += valid ? 1u : 0u;
+                    // settled iff (|a|^2+|b|^2)(1-eps) - 2G >= max(dv)(1+eps_h) + tiny (tc_pairs.cuh)
+                    const float lhs = fmaf(-2.0f, __uint_as_float(r[c]), abi.x + ax);
+                    const float rhs = abi.y >= ay ? abi.y : ay;
+                    cm |= (valid && !(lhs >= rhs)) ? (1u << c) : 0u;
+                }
+                if (__any_sync(FULL, cm != 0u)) {
+                    const int n = __popc(cm);
+                    int qi = n ? atomicAdd(&sm.qn[b], n) : 0;
+                    while (cm) {
+                        const int c = __ffs(cm) - 1;
+                        cm &= cm - 1u;
+                        const int jr = cb + c;
+                        if (qi < S::QC) sm.q[b][qi] = tr ? (uint32_t)((jr << 8) | i) : (uint32_t)((i << 8) | jr);
+                        ++qi;
+                    }
+                }
+            };
+            if (GP == 1) {
+                // upper-triangle 32x32 blocks (a, b'), a <= b' < 3, two per warp: (fw, fw) and
+                // (fw, fw+1); warp 2 takes (0, 2) as its transpose (rows 64.., columns 0..31)
+                const int c0 = fw * 32, c1 = fw < 2 ? fw * 32 + 32 : 0;
+                const bool t1 = fw == 2;
+#pragma unroll 1
+                for (int h = 0; h < 4; ++h) {  // warp-uniform
+                    const int cb = (h < 2 ? c0 : c1) + (h & 1) * 16;
+                    if (cb >= kcols) continue;
+                    scan16(cb, h >= 2 && t1);
+                }
+            } else {
+                const int c_lo = ((fw * 32) / SZ) * SZ, c_hi = ((fw * 32 + 31) / SZ + 1) * SZ;
+                const int start = ((c_lo >> 4) << 4) > fw * 32 ? ((c_lo >> 4) << 4) : fw * 32;
+#pragma unroll 1
+                for (int cb = start; cb < c_hi; cb += 16) scan16(cb, false);  // warp-uniform
+            }
+            st_pairs += np;
+            tc::fence_before();
+            if (tid == 128) T3P_EV(g, 5);
+            tc::mbar_arrive(&sm.acce[b]);
+            tc::mbar_arrive(&sm.qrdy[b]);
+        }
+    } else {
+        // ================= exact chains + write-out (warps 2, 3, 7) =================
+        const int et = warp == 7 ? 64 + lane : (warp - 2) * 32 + lane;  // 0..95
+        constexpr int NE = 96;
+        auto exact2 = [&](const unsigned char *stg, int i1, int j1, int i2, int j2, float &d1, float &d2) {
+            float s1 = 0.0f, s2 = 0.0f;
+#pragma unroll 4
+            for (int c = 0; c < nq; ++c) {
+                const float4 x1 = *reinterpret_cast<const float4 *>(stg + t3_off(i1, c));
+                const float4 y1 = *reinterpret_cast<const float4 *>(stg + t3_off(j1, c));
+                const float4 x2 = *reinterpret_cast<const float4 *>(stg + t3_off(i2, c));
+                const float4 y2 = *reinterpret_cast<const float4 *>(stg + t3_off(j2, c));
+                s1 = exact_step(s1, x1.x, y1.x);
+                s2 = exact_step(s2, x2.x, y2.x);
+                s1 = exact_step(s1, x1.y, y1.y);
+                s2 = exact_step(s2, x2.y, y2.y);
+                s1 = exact_step(s1, x1.z, y1.z);
+                s2 = exact_step(s2, x2.z, y2.z);
+                s1 = exact_step(s1, x1.w, y1.w);
+                s2 = exact_step(s2, x2.w, y2.w);
+            }
+            d1 = s1;
+            d2 = s2;
+        };
+        for (int64_t g = 0; g < nmine; ++g) {
+            const int s = (int)(g % NS), m = (int)(g % NM), b = (int)(g & 1);
+            const unsigned char *stg = base + s * T3_STAGE;
+            const T3Meta &mt = sm.meta[m];
+            T3P_WAIT(9, tc::mbar_wait(&sm.qrdy[b], (uint32_t)((g >> 1) & 1)));
+            auto record = [&](int i, int j, float d) {  // pair of group rows i < j, same pool
+                const int p = i / SZ;
+                const int x1 = mt.pos[i], x2 = mt.pos[j];
+                const float d1 = mt.dv[i], d2 = mt.dv[j];
+                const int xa = x1 < x2 ? x1 : x2, xb = x1 < x2 ? x2 : x1;
+                const float dva = x1 < x2 ? d1 : d2, dvb = x1 < x2 ? d2 : d1;
+                const unsigned long long bit = 1ull << (xb & 63);
+                atomicOr((unsigned long long *)&sm.cond[p * SZ + xa][xb >> 6], bit);
+                if (!(dvb >= dva)) atomicOr((unsigned long long *)&sm.afar[p * SZ + xa][xb >> 6], bit);
+                const int c = atomicAdd(&sm.cl_n[b][p], 1);
+                if (c < S::CL) {
+                    sm.cl_key[p][c] = (uint32_t)((xa << 8) | xb);
+                    sm.cl_d[p][c] = d;
+                }
+            };
+            const int qn = sm.qn[b];
+            if (et == 0) T3P_EV(g, 6);
+            if (et == 0) {
+                st_cand += (unsigned long long)qn;
+                st_ovf += qn > S::QC ? 1ull : 0ull;
+            }
+            if (qn <= S::QC) {
+                for (int e = et; e < qn; e += 2 * NE) {
+                    const bool two = e + NE < qn;
+                    const uint32_t k1 = sm.q[b][e], k2 = two ? sm.q[b][e + NE] : k1;
+                    const int i1 = (int)(k1 >> 8), j1 = (int)(k1 & 255u), i2 = (int)(k2 >> 8), j2 = (int)(k2 & 255u);
+                    float x1, x2;
+                    exact2(stg, i1, j1, i2, j2, x1, x2);
+                    const float a1 = mt.dv[i1], b1 = mt.dv[j1];
+                    if (x1 < (a1 >= b1 ? a1 : b1)) record(i1, j1, x1);
+                    const float a2 = mt.dv[i2], b2 = mt.dv[j2];
+                    if (two && x2 < (a2 >= b2 ? a2 : b2)) record(i2, j2, x2);
+                }
+            } else {
+                // queue overflow (degenerate data or the first rounds): exact sweep of every pair
+#pragma unroll 1
+                for (int pp = 0; pp < GP; ++pp) {
+                    const int k = mt.hdr[pp].y;
+                    const int npairs = k * (k - 1) / 2;
+                    for (int t = et; t < npairs; t += 2 * NE) {
+                        const bool two = t + NE < npairs;
+                        int s1, u1, s2 = 0, u2 = 0;
+                        tile_decode(t, s1, u1);
+                        if (two) tile_decode(t + NE, s2, u2);
+                        const int i1 = pp * SZ + s1, j1 = pp * SZ + u1 + 1;
+                        const int i2 = two ? pp * SZ + s2 : i1, j2 = two ? pp * SZ + u2 + 1 : j1;
+                        float x1, x2;
+                        exact2(stg, i1, j1, i2, j2, x1, x2);
+                        const float a1 = mt.dv[i1], b1 = mt.dv[j1];
+                        if (mt.ids[i1] != TOMB && mt.ids[j1] != TOMB && x1 < (a1 >= b1 ? a1 : b1)) record(i1, j1, x1);
+                        const float a2 = mt.dv[i2], b2 = mt.dv[j2];
+                        if (two && mt.ids[i2] != TOMB && mt.ids[j2] != TOMB && x2 < (a2 >= b2 ? a2 : b2))
+                            record(i2, j2, x2);
+                    }
+                }
+            }
+            T3P_WAIT(10, tc::named_bar(2, 96));  // masks + kept distances of group g complete
+            // the stage's rows are no longer read: let the producers refill it
+            tc::mbar_arrive(&sm.empty[s]);
+            for (int e = et; e < R * mw; e += NE) {
+                const int r = mw == 2 ? e >> 1 : e, wd = mw == 2 ? e & 1 : 0;
+                const int pp = r / SZ, x = r - pp * SZ;
+                const int64_t v = mt.hdr[pp].x;
+                if (v < 0 || x >= mt.hdr[pp].y - 1) continue;
+                const uint64_t cv = sm.cond[r][wd], fv = sm.afar[r][wd];
+                sm.cond[r][wd] = 0ull;
+                sm.afar[r][wd] = 0ull;
+                a.w.cond[(v * cap + x) * mw + wd] = cv;
+                a.w.afar[(v * cap + x) * mw + wd] = fv;
+            }
+            const int lcap = S::CL < 4 * cap ? S::CL : 4 * cap;
+            for (int e = et; e < GP * S::CL; e += NE) {
+                const int pp = e / S::CL, c = e - pp * S::CL;
+                const int64_t v = mt.hdr[pp].x;
+                if (v < 0) continue;
+                const int ncl = sm.cl_n[b][pp];
+                const int nw = ncl < lcap ? ncl : lcap;
+                if (c == 0) {
+                    a.w.cl_n[v] = nw;  // truncated lists: decide re-evaluates misses
+                    st_red += (unsigned long long)ncl;
+                }
+                if (c < nw) {
+                    a.w.cl[v * 4 * (int64_t)cap + c] = sm.cl_key[pp][c];
+                    a.w.cl_d[v * 4 * (int64_t)cap + c] = sm.cl_d[pp][c];
+                }
+            }
+            tc::named_bar(2, 96);  // masks / counters / metadata read: reset for the next groups
+            if (et == 0) {
+                sm.qn[b] = 0;
+#pragma unroll
+                for (int p = 0; p < GP; ++p) sm.cl_n[b][p] = 0;
+            }
+            if (et == 0) T3P_EV(g, 7);
+            tc::mbar_arrive(&sm.qemp[b]);
+            tc::mbar_arrive(&sm.mempty[m]);
+        }
+    }
+#ifdef GRNND_T3_PROF
+    if (lane == 0) T3P_ADD(warp == 0 ? 1 : warp == 1 ? 17 : (warp >= 4 && warp <= 6) ? 8 : warp >= 8 ? 14 : 11, _t3p0);
+    if (tid == 0) atomicAdd(&g_t3prof[12], (unsigned long long)nmine);
+#endif
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 1) tc::tmem_dealloc(tmem, TC_TMEM_COLS);
+    if (a.stats) {
+        st_pairs = warp_sum(st_pairs);
+        st_red = warp_sum(st_red);
+        if (lane == 0 && st_pairs) atomicAdd((unsigned long long *)&a.stats[GRNND_ST_PAIRS], st_pairs);
+        if (lane == 0 && st_red) atomicAdd((unsigned long long *)&a.stats[GRNND_ST_REDIRECTABLE], st_red);
+        if (st_cand) atomicAdd((unsigned long long *)&a.stats[GRNND_ST_CANDIDATES], st_cand);
+        if (st_ovf) atomicAdd((unsigned long long *)&a.stats[GRNND_ST_OVERFLOWS], st_ovf);
+    }
+}
+
+// Lays out the metadata of every TC group contiguously (staging slot e = group * 96 + row):
+// pool id, stored distance, permutation position, row norm; plus per group the (vertex, k)
+// of its pools.  Thread per staging slot: reads of a pool's row are coalesced.
+__global__ void tc_stage_kernel(PropArgs a) {
+    const unsigned long long *ctr = a.w.ctr;
+    int64_t gb[7];
+    gb[1] = 0;
+    for (int b = 1; b <= 5; ++b) gb[b + 1] = gb[b] + ((int64_t)ctr[C_BIN0 + b] + tc_bin_gp(b) - 1) / tc_bin_gp(b);
+    const int64_t total = gb[6] * T3_ROWS;
+    const int cap = a.cap, pcap = a.w.pcap;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t grp = e / T3_ROWS;
+        const int r = (int)(e - grp * T3_ROWS);
+        int b = 1;
+        while (b < 5 && grp >= gb[b + 1]) ++b;
+        const int sz = tc_bin_sz(b), gp = tc_bin_gp(b);
+        const int p = r / sz, s = r - p * sz;
+        const int64_t posn = (grp - gb[b]) * gp + p;  // position in bin b's list
+        int2 vk = make_int2(-1, 0);
+        if (posn < (int64_t)ctr[C_BIN0 + b]) vk = a.w.bins[(int64_t)b * a.w.n + posn];
+        int32_t id = TOMB;
+        float dv = 0.0f, nr = 0.0f;
+        uint8_t ps = 0;
+        if (s < vk.y) {
+            const int64_t off = (int64_t)vk.x * cap + s;
+            id = a.read_ids[off];
+            dv = a.read_dists[off];
+            ps = a.w.pos8[(int64_t)vk.x * pcap + s];
+            nr = a.norms[id];
+        }
+        a.w.s_ids[e] = id;
+        a.w.s_dv[e] = dv;
+        a.w.s_nrm[e] = nr;
+        a.w.s_pos[e] = ps;
+        if (s == 0) a.w.s_hdr[grp * 8 + p] = vk;
+    }
+}

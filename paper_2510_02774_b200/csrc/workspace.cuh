@@ -7,7 +7,7 @@
 
 namespace grnnd {
 
-constexpr int NBINS = 6;  // propagate bins by live count k: see propagate.cu
+constexpr int NBINS = 8;  // propagate bins by live count k: see propagate.cu
 constexpr int HEAVY_SEG = 32;  // segments longer than this are sorted by a CTA
 
 // small counters block (unsigned long long so atomicAdd works on it)
@@ -49,6 +49,13 @@ struct Workspace {
     int32_t *cl_n;       // [n] redirect-capable pairs found (may exceed the list)
     uint32_t *cl;        // [n, 4*cap] (key << 16 | ...) packed: key in high 16 bits of the slot
     float *cl_d;         // [n, 4*cap] their exact distances
+    // tensor-core pair phase (tc3_pairs.cuh): group metadata staged contiguously, 96 slots
+    // per group (only carved when cap <= 96)
+    int32_t *s_ids;
+    float *s_dv;
+    float *s_nrm;
+    uint8_t *s_pos;
+    int2 *s_hdr;         // [groups, 8] (vertex row, k) per pool
     int64_t n;
     int64_t msg_capacity;
 };
@@ -97,6 +104,12 @@ inline size_t carve(Workspace *w, void *base, int64_t n, int32_t cap, int64_t ms
     t.cl_n = (int32_t *)take(4 * N);
     t.cl = (uint32_t *)take(4 * N * 4 * (size_t)(cap > 0 ? cap : 1));
     t.cl_d = (float *)take(4 * N * 4 * (size_t)(cap > 0 ? cap : 1));
+    const size_t SG = (cap > 0 && cap <= 96) ? N + 8 : 1;  // staging groups (<= one per pool + bins)
+    t.s_ids = (int32_t *)take(4 * SG * 96);
+    t.s_dv = (float *)take(4 * SG * 96);
+    t.s_nrm = (float *)take(4 * SG * 96);
+    t.s_pos = (uint8_t *)take(SG * 96);
+    t.s_hdr = (int2 *)take(8 * 8 * SG);
     t.n = n;
     t.msg_capacity = msg_capacity;
     if (w) *w = t;

@@ -80,7 +80,7 @@ class ShardPools(_DevicePools):
 
     def emit(self, kind: int, seed: int, stream_id: int, order: int, rho: float, bounds_dev: torch.Tensor,
              stats: torch.Tensor) -> None:
-        p = self.struct(stats)
+        p = self.struct(stats, kind != 0 or self.filtered_round(stream_id))
         _lib.call("grnnd_round_emit", C.byref(p), kind, seed & MASK64, stream_id & MASK64, order, float(rho),
                   bounds_dev.data_ptr(), self.world, self.send_counts.data_ptr(), _stream(self.dev))
 

@@ -343,3 +343,15 @@ def test_filter_degenerate_ties_and_large_norms(g, dim):
         graph = g.build(g.Dataset(x), g.BuildParams(S=16, R=96, T1=2, T2=3, rho=0.6, seed=4))
         off, nb = oracle.build(x, 16, 96, 2, 3, 0.6, 4)
         assert np.array_equal(graph.offsets, off) and np.array_equal(graph.neighbor_ids, nb)
+
+
+def test_filtered_phase_from_the_first_round(g, monkeypatch):
+    """Filtered pair phase from round 1 (random pools: most pairs are candidates, the
+    tensor-core path's candidate queues overflow into exact sweeps) -- same graph."""
+    monkeypatch.setenv("GRNND_EXACT_FIRST_ROUNDS", "0")
+    for n, dim, dist, R, seed in [(20000, 128, "gaussian", 96, 1), (6000, 100, "clustered", 64, 2),
+                                  (5000, 128, "gaussian", 40, 3)]:
+        ds = generate(n, dim, dist, seed=seed)
+        graph = g.build(ds, g.BuildParams(S=20 if R > 20 else 16, R=R, T1=2, T2=4, rho=0.6, seed=seed))
+        off, nb = oracle.build(ds.data, 20 if R > 20 else 16, R, 2, 4, 0.6, seed)
+        assert np.array_equal(graph.offsets, off) and np.array_equal(graph.neighbor_ids, nb), (n, dim, dist, R)

@@ -33,4 +33,8 @@ for rep in range(2):
     r = rows.cpu().numpy()
     print(f"rep {rep}: wall {t1_ - t0:.3f}s  rounds+finalize device {sum(per):.1f} ms")
     print("  per-round ms:", " ".join(f"{x:.1f}" for x in per))
-    print("  pairs total %.3e  pairs_ref %.3e  sum_k %.3e" % (r[:, 8].sum(), r[:, 9].sum(), r[:, 0].sum()))
+    print("  pairs total %.3e  pairs_ref %.3e  sum_k %.3e  candidates %.3e (%.2f%%)  overflows %d" % (
+        r[:, 8].sum(), r[:, 9].sum(), r[:, 0].sum(), r[:, 10].sum(), 100 * r[:, 10].sum() / max(r[:, 8].sum(), 1),
+        r[:, 11].sum()))
+    print("  redirect-capable pairs %.3e (%.3f%% of pairs)" % (r[:, 12].sum(), 100 * r[:, 12].sum() / max(r[:, 8].sum(), 1)))
+    print("  per-round candidates %:", " ".join(f"{100 * a / max(b, 1):.2f}" for a, b in zip(r[:, 10], r[:, 8])))

@@ -1,0 +1,36 @@
+"""Role timers + CTA-0 event trace of tc3_pairs_kernel (GRNND_T3_PROF build), one mid-build round."""
+import ctypes as C, sys
+sys.path.insert(0, ".")
+import numpy as np
+import torch
+import paper_2510_02774_b200 as g
+from paper_2510_02774_b200 import _lib
+lib = _lib.lib
+lib.grnnd_debug_counters.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+lib.grnnd_debug_trace.argtypes = [C.POINTER(C.c_longlong)]
+ds = g.generate(1_000_000, 128, "gaussian", seed=1)
+p = g.BuildParams(S=20, R=96, T1=2, T2=15, rho=0.6, seed=1)
+st = g.init_neighbors(ds, p)
+row = torch.zeros(16, dtype=torch.int64, device="cuda")
+buf = (C.c_ulonglong * 32)()
+# slot, name, number of timed warps (lane 0 of each)
+rows = [(0, "meta wait mempty", 1), (1, "meta total", 1), (2, "mma wait full", 1), (3, "mma wait acce", 1),
+        (17, "mma total", 1), (4, "filt wait mfull", 3), (5, "filt bar1", 3), (6, "filt wait qemp", 3),
+        (7, "filt wait accf", 3), (8, "filt total", 3), (9, "exact wait qrdy", 3), (10, "exact bar2", 3),
+        (11, "exact total", 3), (15, "rows wait mfull", 12), (16, "rows wait empty", 12), (14, "rows total", 12)]
+for r in range(25):
+    st.pools.update(p.seed, 1 + st.round_index, 0, row); st.round_index += 1
+    torch.cuda.synchronize()
+    lib.grnnd_debug_counters(buf, 32)
+    if r in (0, 24):
+        v = list(buf)
+        print(f"round {r + 1}: groups {v[12]}")
+        for slot, name, w in rows:
+            print(f"   {name:22s} {v[slot] / max(v[12], 1) / w:10.0f} cycles/group")
+tr = (C.c_longlong * 512)()
+lib.grnnd_debug_trace(tr)
+t = np.array(list(tr)).reshape(64, 8)
+t0 = t[0, 0]
+print("events (K cycles; CTA 0 of the last bin kernel): 0 meta issued, 1 rows issued, 3 mma issued, 4 filter start, 5 filter done, 6 exact start, 7 exact done")
+for gi in range(0, 24):
+    print(gi, " ".join(f"{(x - t0) / 1000:8.1f}" for x in t[gi]))
