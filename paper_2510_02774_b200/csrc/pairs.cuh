@@ -11,7 +11,7 @@
 template <int MAXK, int B>
 struct PairSmem {
     static constexpr int W = (MAXK + 63) / 64;  // 64-bit words per mask row
-    static constexpr int CL = 64;  // redirect-capable pairs kept (~0.02% of pairs; overflow re-evaluated)
+    static constexpr int CL = PAIR_LIST;  // redirect-capable pairs handed to decide (workspace.cuh)
     uint64_t cond[B][MAXK * W];
     uint64_t afar[B][MAXK * W];
     int32_t ids[2][B][MAXK];  // pool rows of the current / next batch
@@ -20,7 +20,7 @@ struct PairSmem {
     float nrm[2][B][MAXK];    // squared norms of the pool members' rows (filtered mode)
     int32_t k[2][B];
     int64_t v[2][B];          // local row of each batch member (-1: none)
-    uint32_t cl_key[B][CL];   // (anchor pos << 8) | partner pos
+    uint32_t cl_key[B][CL];   // (afar << 16) | (anchor pos << 8) | partner pos
     float cl_d[B][CL];
     int cl_n[B];
     int tp[B + 1];            // tile prefix over the batch members
@@ -41,11 +41,12 @@ __device__ __forceinline__ void record_redirect(PairSmem<MAXK, B> &sm, int cur, 
     const int xa = x1 < x2 ? x1 : x2, xb = x1 < x2 ? x2 : x1;
     const float dva = x1 < x2 ? d1 : d2, dvb = x1 < x2 ? d2 : d1;
     const unsigned long long bit = 1ull << (xb & 63);
+    const bool far = !(dvb >= dva);
     atomicOr((unsigned long long *)&sm.cond[g][xa * W + (xb >> 6)], bit);
-    if (!(dvb >= dva)) atomicOr((unsigned long long *)&sm.afar[g][xa * W + (xb >> 6)], bit);
+    if (far) atomicOr((unsigned long long *)&sm.afar[g][xa * W + (xb >> 6)], bit);
     const int c = atomicAdd(&sm.cl_n[g], 1);
     if (c < S::CL) {
-        sm.cl_key[g][c] = (uint32_t)((xa << 8) | xb);
+        sm.cl_key[g][c] = (uint32_t)((far ? 1u << 16 : 0u) | (xa << 8) | xb);
         sm.cl_d[g][c] = d;
     }
 }
@@ -365,20 +366,23 @@ __global__ void __launch_bounds__(THREADS) pairs_kernel(PropArgs a, int bin, int
             const int64_t v = sm.v[cur][g];
             if (v < 0) continue;
             const int k = sm.k[cur][g];
-            uint64_t *gc = a.w.cond + v * (int64_t)cap * mw;
-            uint64_t *ga = a.w.afar + v * (int64_t)cap * mw;
-            for (int e = tid; e < (k - 1) * mw; e += THREADS) {
-                const int x = e / mw, wd = e - x * mw;
-                gc[e] = wd < W ? sm.cond[g][x * W + wd] : 0ull;
-                ga[e] = wd < W ? sm.afar[g][x * W + wd] : 0ull;
-            }
-            const int lcap = S::CL < 4 * cap ? S::CL : 4 * cap;
             const int ncl = sm.cl_n[g];
+            const int lcap = list_cap(cap);
+            if (ncl > lcap) {  // incomplete list: the masks go to global too
+                uint64_t *gc = a.w.cond + v * (int64_t)cap * mw;
+                uint64_t *ga = a.w.afar + v * (int64_t)cap * mw;
+                for (int e = tid; e < (k - 1) * mw; e += THREADS) {
+                    const int x = e / mw, wd = e - x * mw;
+                    gc[e] = wd < W ? sm.cond[g][x * W + wd] : 0ull;
+                    ga[e] = wd < W ? sm.afar[g][x * W + wd] : 0ull;
+                }
+            }
             const int nw = ncl < lcap ? ncl : lcap;
-            if (tid == 0) a.w.cl_n[v] = nw;  // truncated lists: decide re-evaluates misses
+            int32_t *rec = a.w.clrec + v * (int64_t)CLREC;
+            if (tid == 0) rec[0] = ncl;
             for (int e = tid; e < nw; e += THREADS) {
-                a.w.cl[v * 4 * (int64_t)cap + e] = sm.cl_key[g][e];
-                a.w.cl_d[v * 4 * (int64_t)cap + e] = sm.cl_d[g][e];
+                rec[4 + 2 * e] = (int32_t)sm.cl_key[g][e];
+                rec[5 + 2 * e] = __float_as_int(sm.cl_d[g][e]);
             }
         }
         __syncthreads();  // per-batch shared state is reused next iteration

@@ -114,6 +114,11 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool va
     const int sz = valid ? 16 : 0;
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
 }
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem, bool valid) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int sz = valid ? 4 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
@@ -217,7 +222,6 @@ __device__ __forceinline__ void tile_dot(float (&acc)[T * T], const float4 *__re
 }
 
 #include "pairs.cuh"
-#include "pairs5.cuh"
 #include "tc_pairs.cuh"
 #include "tc3_pairs.cuh"
 
@@ -283,15 +287,45 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) decide_kernel(PropArgs a) {
         }
         const uint64_t *gc = a.w.cond + v * (int64_t)cap * MW;
         const uint64_t *ga = a.w.afar + v * (int64_t)cap * MW;
+        // redirect-capable pairs (workspace.cuh PAIR_LIST): a complete list replaces the masks
+        const int lcap = list_cap(cap);
+        const int32_t *rec = a.w.clrec + v * (int64_t)CLREC;
+        const int ncl_all = rec[0];
+        const bool from_list = ncl_all <= lcap;
+        const int ncl = ncl_all < lcap ? ncl_all : lcap;
+        int2 e0 = make_int2(0, 0), e1 = make_int2(0, 0);
+        if (lane < ncl) e0 = *reinterpret_cast<const int2 *>(rec + 4 + 2 * lane);
+        if (lane + 32 < ncl) e1 = *reinterpret_cast<const int2 *>(rec + 4 + 2 * (lane + 32));
+        const uint32_t key0 = (uint32_t)e0.x, key1 = (uint32_t)e1.x;
+        const float cd0 = __int_as_float(e0.y), cd1 = __int_as_float(e1.y);
         int nm = 0;
         unsigned long long refp = 0;
         for (int x0 = 0; x0 < k - 1; x0 += 32) {
             const int x = x0 + lane;
             uint64_t c[MW], am[MW];
+            if (from_list) {
 #pragma unroll
-            for (int i = 0; i < MW; ++i) {
-                c[i] = x < k - 1 ? gc[x * MW + i] : 0ull;
-                am[i] = x < k - 1 ? ga[x * MW + i] : 0ull;
+                for (int i = 0; i < MW; ++i) c[i] = am[i] = 0ull;
+                for (int t = 0; t < ncl; ++t) {
+                    const uint32_t kk = __shfl_sync(FULL, t < 32 ? key0 : key1, t & 31);
+                    if ((int)((kk >> 8) & 255u) == x) {
+                        const int xb = (int)(kk & 255u);
+                        const uint64_t bit = 1ull << (xb & 63);
+#pragma unroll
+                        for (int i = 0; i < MW; ++i) {
+                            if (i == (xb >> 6)) {
+                                c[i] |= bit;
+                                if (kk >> 16) am[i] |= bit;
+                            }
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < MW; ++i) {
+                    c[i] = x < k - 1 ? gc[x * MW + i] : 0ull;
+                    am[i] = x < k - 1 ? ga[x * MW + i] : 0ull;
+                }
             }
             int cur = x0;
             while (true) {
@@ -373,28 +407,18 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) decide_kernel(PropArgs a) {
             if (lane == 0) base = atomicAdd(&a.w.ctr[C_LIST], (unsigned long long)nm);
             base = __shfl_sync(FULL, base, 0);
         }
-        const int lcap = 4 * cap;
-        const int ncl_raw = nm > 0 ? a.w.cl_n[v] : 0;
-        const int ncl = ncl_raw < lcap ? ncl_raw : lcap;
-        const uint32_t *clk = a.w.cl + v * (int64_t)lcap;
-        const float *cld = a.w.cl_d + v * (int64_t)lcap;
         for (int jb = 0; jb < nm; jb += 32) {
             const int j = jb + lane;
             const uint32_t mykey = j < nm ? (uint32_t)sm.e_key[wib][j] : 0xFFFFFFFFu;
-            // the pairs kernel kept every redirect-capable pair's exact distance: warp search
+            // the pair phase kept every redirect-capable pair's exact distance: warp search
             float d = 0.0f;
             bool found = false;
-            for (int c0 = 0; c0 < ncl; c0 += 32) {
-                const uint32_t ck = c0 + lane < ncl ? clk[c0 + lane] : 0xFFFFFFFEu;
-                const float cd = c0 + lane < ncl ? cld[c0 + lane] : 0.0f;
-                const int nc = ncl - c0 < 32 ? ncl - c0 : 32;
-                for (int t = 0; t < nc; ++t) {
-                    const uint32_t kk = __shfl_sync(FULL, ck, t);
-                    const float dd = __shfl_sync(FULL, cd, t);
-                    if (kk == mykey) {
-                        d = dd;
-                        found = true;
-                    }
+            for (int t = 0; t < ncl; ++t) {
+                const uint32_t kk = __shfl_sync(FULL, t < 32 ? key0 : key1, t & 31) & 0xFFFFu;
+                const float dd = __shfl_sync(FULL, t < 32 ? cd0 : cd1, t & 31);
+                if (kk == mykey) {
+                    d = dd;
+                    found = true;
                 }
             }
             if (j >= nm) continue;
@@ -538,22 +562,6 @@ static int launch_pairs(const PropArgs &a, int bin, cudaStream_t st) {
     return launch_pairs_mode<MAXK, B, THREADS, TPT, T, false>(a, bin, st);
 }
 
-template <int MAXK, int B, int NW, int T, bool BLOCKED>
-static int launch_pairs5(const PropArgs &a, int bin, cudaStream_t st) {
-    const int nq = (a.dim + 3) >> 2;
-    auto kern = nq == 32 ? pairs5_kernel<MAXK, B, NW, T, BLOCKED, 32> : pairs5_kernel<MAXK, B, NW, T, BLOCKED, 0>;
-    const int kmax = ((MAXK < a.cap ? MAXK : a.cap) + T - 1) / T * T;
-    const size_t smem = align_up(sizeof(P5Smem<MAXK, B>), 128) + (size_t)2 * B * kmax * P5_RS4 * 16;
-    GRNND_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    GRNND_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NW * 32, smem));
-    if (per_sm < 1) {
-        set_error("pairs5 bin %d: no CTA fits (smem %zu B)", bin, smem);
-        return GRNND_EUNSUPPORTED;
-    }
-    kern<<<sm_count() * per_sm, NW * 32, smem, st>>>(a, bin, kmax);
-    return check_launch("pairs5_kernel");
-}
 
 template <int SZ>
 static int launch_tc_pairs(const PropArgs &a, int bin, cudaStream_t st) {
@@ -585,9 +593,6 @@ static int launch_tc3_pairs(const PropArgs &a, int bin, cudaStream_t st) {
 #define GRNND_TC 1  // tensor-core Gram pre-screen (tc_pairs.cuh) for D <= 128, R <= 128
 #endif
 
-#ifndef GRNND_P5
-#define GRNND_P5 0  // pipelined CUDA-core variant: measured slower, kept for A/B
-#endif
 
 int launch_propagate(const PropArgs &a, cudaStream_t st) {
     const int64_t n = a.hi - a.lo;
@@ -615,13 +620,6 @@ int launch_propagate(const PropArgs &a, cudaStream_t st) {
         if (a.cap > 32) GRNND_TRY(launch_tc_pairs<64>(a, 3, st));
         if (a.cap > 16) GRNND_TRY(launch_tc_pairs<32>(a, 2, st));
         if (a.cap > 1) GRNND_TRY(launch_tc_pairs<16>(a, 1, st));
-    } else if (GRNND_P5 && a.norms && a.dim <= 128 && a.cap <= 128) {
-        // pipelined filtered pair phase (pairs5.cuh)
-        if (a.cap > 64 && a.cap <= 96) GRNND_TRY((launch_pairs5<96, 1, 4, 4, true>(a, 4, st)));
-        if (a.cap > 96) GRNND_TRY((launch_pairs5<128, 1, 4, 4, true>(a, 4, st)));
-        if (a.cap > 32) GRNND_TRY((launch_pairs5<64, 1, 4, 2, true>(a, 3, st)));
-        if (a.cap > 16) GRNND_TRY((launch_pairs5<32, 2, 4, 2, false>(a, 2, st)));
-        if (a.cap > 1) GRNND_TRY((launch_pairs5<16, 4, 4, 2, false>(a, 1, st)));
     } else {
     // k in (64, 96] with R <= 96 (the benchmark shape): a slab sized for 96 rows fits four
     // CTAs per SM where the 128-row one fits three

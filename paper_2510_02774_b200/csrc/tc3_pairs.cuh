@@ -10,7 +10,7 @@
 //     ids, stored distances, permutation positions, row norms, (vertex, k) header);
 //   warp 0       metadata: one thread streams group g's metadata into meta slot g % 8 with
 //                1-D bulk copies (TMA), completing on mfull[m];
-//   warps 8-19   row producers: cp.async of the 96 vector rows into stage g % 4 (K-major,
+//   warps 11-19  row producers: cp.async of the 96 vector rows into stage g % 4 (K-major,
 //                128-byte swizzle); completion arrives on full[s] in hardware
 //                (cp.async.mbarrier.arrive.noinc).  Random 512-byte row gathers need ~16
 //                issuing warps per SM to approach HBM bandwidth (a warp's cp.async stream is
@@ -19,8 +19,8 @@
 //   warp 1       MMA: one thread fences the async proxy and issues the 16 MMAs of group g
 //                into TMEM accumulator g % 2;
 //   warps 4-6    filter (TMEM lanes 0..95): Gram -> band candidates -> queue g % 2;
-//   warps 2,3,7  exact chains of the queue -> redirect masks -> global; release the stage
-//                and the meta slot.
+//   warps 2,3,7 / 8,9,10  two exact sets (even / odd groups): exact chains of the queue ->
+//                redirect records -> global (bulk stores); release the stage and meta slot.
 // Groups: 96 rows = one pool of k <= 96, or 96/SZ pools of k <= SZ (SZ = 16, 24, 32, 48).
 #pragma once
 
@@ -28,10 +28,10 @@ constexpr int T3_ROWS = 96;
 constexpr int T3_KB = T3_ROWS * 128;  // one 32-dim k-block of a stage (12 KB)
 constexpr int T3_STAGE = 4 * T3_KB;   // 96 rows x 128 fp32 (48 KB)
 constexpr int T3_NS = 4;              // row stages
-constexpr int T3_NM = 8;              // metadata slots
+constexpr int T3_NM = 6;              // metadata slots
 constexpr int T3_PAD = 4096;          // the M = 128 MMA reads 32 rows past the last k-block
 constexpr int T3_NT = 640;            // 20 warps
-constexpr int T3_NP = 12;             // row-producer warps (8..19)
+constexpr int T3_NP = 9;              // row-producer warps (11..19)
 
 struct T3Meta {  // one group's metadata, filled by bulk copies from the staging arrays
     int32_t ids[T3_ROWS];
@@ -45,14 +45,13 @@ constexpr uint32_t T3_META_BYTES = 3 * 4 * T3_ROWS + T3_ROWS + 64;
 template <int SZ>
 struct T3Smem {
     static constexpr int GP = T3_ROWS / SZ;
-    static constexpr int CL = 64;    // kept redirect distances per pool
-    static constexpr int QC = 1024;  // filter candidates per group (overflow: exact sweep)
+    static constexpr int CL = PAIR_LIST;  // redirect-capable pairs handed to decide (workspace.cuh)
+    static constexpr int QC = 512;   // filter candidates per group (overflow: exact sweep)
     T3Meta meta[T3_NM];
     float2 ab[2][T3_ROWS];        // filter terms (A = -inf: always a candidate; B = -1: dead row)
-    uint64_t cond[T3_ROWS][2];    // row = p * SZ + anchor position; bit = partner position
-    uint64_t afar[T3_ROWS][2];
-    uint32_t cl_key[GP][CL];
-    float cl_d[GP][CL];
+    uint64_t cond[2][T3_ROWS][2];  // per exact set: row = p * SZ + anchor position; bit = partner
+    uint64_t afar[2][T3_ROWS][2];
+    alignas(16) int32_t rec[2][GP][CLREC];  // per exact set, per pool: pair records (workspace.cuh)
     int cl_n[2][GP];
     int qn[2];
     uint32_t q[2][QC];            // (row i << 8) | row j
@@ -145,9 +144,9 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
         }
         tc::fence_mbar_init();
     }
-    for (int i = tid; i < R * 2; i += T3_NT) {
-        (&sm.cond[0][0])[i] = 0ull;
-        (&sm.afar[0][0])[i] = 0ull;
+    for (int i = tid; i < 2 * R * 2; i += T3_NT) {
+        (&sm.cond[0][0][0])[i] = 0ull;
+        (&sm.afar[0][0][0])[i] = 0ull;
     }
     if (tid < 2) sm.qn[tid] = 0;
     if (tid < 2 * GP) (&sm.cl_n[0][0])[tid] = 0;
@@ -177,11 +176,11 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             }
         }
         __syncwarp();
-    } else if (warp >= 8) {
-        // ================= row producers (12 warps) =================
-        // warp pi stages group rows pi, pi + 12, ..: one 512-byte row per instruction (lane =
+    } else if (warp >= 11) {
+        // ================= row producers (9 warps) =================
+        // warp pi stages group rows pi, pi + 9, ..: one 512-byte row per instruction (lane =
         // 16-byte chunk, 128-byte swizzle)
-        const int pi = warp - 8;
+        const int pi = warp - 11;
         const bool cv = lane < nq;
         const uint32_t lo = (uint32_t)((lane >> 3) * T3_KB), lx = (uint32_t)(lane & 7);
         for (int64_t g = 0; g < nmine; ++g) {
@@ -190,8 +189,9 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             T3P_WAIT(16, tc::mbar_wait(&sm.empty[s], (uint32_t)(((g / NS) & 1) ^ 1)));
             const uint32_t stg = tc::smem_u32(base + s * T3_STAGE);
 #pragma unroll
-            for (int q = 0; q < R / T3_NP; ++q) {
+            for (int q = 0; q < (R + T3_NP - 1) / T3_NP; ++q) {
                 const int r = pi + T3_NP * q;
+                if (r >= R) break;
                 const int32_t id = sm.meta[m].ids[r];
                 if (id == TOMB) continue;  // empty slot (warp-uniform)
                 const float *src = a.data + (int64_t)id * a.ld + (cv ? lane * 4 : 0);
@@ -312,8 +312,12 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             tc::mbar_arrive(&sm.qrdy[b]);
         }
     } else {
-        // ================= exact chains + write-out (warps 2, 3, 7) =================
-        const int et = warp == 7 ? 64 + lane : (warp - 2) * 32 + lane;  // 0..95
+        // ================= exact chains + write-out: two sets of 3 warps =================
+        // set E (warps 2, 3, 7 / 8, 9, 10) takes the groups g = E mod 2, so the chains (~600+
+        // cycles of dependent adds) and write-out of one group overlap the next group's
+        const int E = warp >= 8 ? 1 : 0;
+        const int et = E ? (warp - 8) * 32 + lane : (warp == 7 ? 64 + lane : (warp - 2) * 32 + lane);  // 0..95
+        const int bar_id = 2 + E;
         constexpr int NE = 96;
         auto exact2 = [&](const unsigned char *stg, int i1, int j1, int i2, int j2, float &d1, float &d2) {
             float s1 = 0.0f, s2 = 0.0f;
@@ -335,7 +339,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             d1 = s1;
             d2 = s2;
         };
-        for (int64_t g = 0; g < nmine; ++g) {
+        for (int64_t g = E; g < nmine; g += 2) {
             const int s = (int)(g % NS), m = (int)(g % NM), b = (int)(g & 1);
             const unsigned char *stg = base + s * T3_STAGE;
             const T3Meta &mt = sm.meta[m];
@@ -347,16 +351,20 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 const int xa = x1 < x2 ? x1 : x2, xb = x1 < x2 ? x2 : x1;
                 const float dva = x1 < x2 ? d1 : d2, dvb = x1 < x2 ? d2 : d1;
                 const unsigned long long bit = 1ull << (xb & 63);
-                atomicOr((unsigned long long *)&sm.cond[p * SZ + xa][xb >> 6], bit);
-                if (!(dvb >= dva)) atomicOr((unsigned long long *)&sm.afar[p * SZ + xa][xb >> 6], bit);
+                const bool far = !(dvb >= dva);
+                atomicOr((unsigned long long *)&sm.cond[b][p * SZ + xa][xb >> 6], bit);
+                if (far) atomicOr((unsigned long long *)&sm.afar[b][p * SZ + xa][xb >> 6], bit);
                 const int c = atomicAdd(&sm.cl_n[b][p], 1);
                 if (c < S::CL) {
-                    sm.cl_key[p][c] = (uint32_t)((xa << 8) | xb);
-                    sm.cl_d[p][c] = d;
+                    sm.rec[b][p][4 + 2 * c] = (int32_t)((far ? 1u << 16 : 0u) | (xa << 8) | xb);
+                    sm.rec[b][p][5 + 2 * c] = __float_as_int(d);
                 }
             };
             const int qn = sm.qn[b];
             if (et == 0) T3P_EV(g, 6);
+#ifdef GRNND_T3_PROF
+            const long long _tx0 = clock64();
+#endif
             if (et == 0) {
                 st_cand += (unsigned long long)qn;
                 st_ovf += qn > S::QC ? 1ull : 0ull;
@@ -396,37 +404,55 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                     }
                 }
             }
-            T3P_WAIT(10, tc::named_bar(2, 96));  // masks + kept distances of group g complete
+#ifdef GRNND_T3_PROF
+            if (lane == 0) T3P_ADD(18, _tx0);
+#endif
+            T3P_WAIT(10, tc::named_bar(bar_id, 96));  // masks + kept distances of group g complete
+#ifdef GRNND_T3_PROF
+            const long long _tx1 = clock64();
+#endif
             // the stage's rows are no longer read: let the producers refill it
             tc::mbar_arrive(&sm.empty[s]);
-            for (int e = et; e < R * mw; e += NE) {
-                const int r = mw == 2 ? e >> 1 : e, wd = mw == 2 ? e & 1 : 0;
+            // pair records -> global by bulk stores (decide_kernel); masks only for incomplete
+            // lists (rare; regular stores); every mask row re-zeroed for the next group
+            const int lcap = list_cap(cap);
+            if (et < GP && mt.hdr[et].x >= 0) {
+                sm.rec[b][et][0] = sm.cl_n[b][et];
+                st_red += (unsigned long long)sm.cl_n[b][et];
+            }
+            for (int e = et; e < R * 2; e += NE) {
+                const int r = e >> 1, wd = e & 1;
                 const int pp = r / SZ, x = r - pp * SZ;
                 const int64_t v = mt.hdr[pp].x;
-                if (v < 0 || x >= mt.hdr[pp].y - 1) continue;
-                const uint64_t cv = sm.cond[r][wd], fv = sm.afar[r][wd];
-                sm.cond[r][wd] = 0ull;
-                sm.afar[r][wd] = 0ull;
-                a.w.cond[(v * cap + x) * mw + wd] = cv;
-                a.w.afar[(v * cap + x) * mw + wd] = fv;
-            }
-            const int lcap = S::CL < 4 * cap ? S::CL : 4 * cap;
-            for (int e = et; e < GP * S::CL; e += NE) {
-                const int pp = e / S::CL, c = e - pp * S::CL;
-                const int64_t v = mt.hdr[pp].x;
-                if (v < 0) continue;
-                const int ncl = sm.cl_n[b][pp];
-                const int nw = ncl < lcap ? ncl : lcap;
-                if (c == 0) {
-                    a.w.cl_n[v] = nw;  // truncated lists: decide re-evaluates misses
-                    st_red += (unsigned long long)ncl;
-                }
-                if (c < nw) {
-                    a.w.cl[v * 4 * (int64_t)cap + c] = sm.cl_key[pp][c];
-                    a.w.cl_d[v * 4 * (int64_t)cap + c] = sm.cl_d[pp][c];
+                const uint64_t cv = sm.cond[b][r][wd], fv = sm.afar[b][r][wd];
+                sm.cond[b][r][wd] = 0ull;
+                sm.afar[b][r][wd] = 0ull;
+                if (v >= 0 && wd < mw && x < mt.hdr[pp].y - 1 && sm.cl_n[b][pp] > lcap) {
+                    a.w.cond[(v * cap + x) * mw + wd] = cv;
+                    a.w.afar[(v * cap + x) * mw + wd] = fv;
                 }
             }
-            tc::named_bar(2, 96);  // masks / counters / metadata read: reset for the next groups
+            tc::fence_proxy_async();  // record stores (generic proxy) -> bulk-store reads (async proxy)
+            tc::named_bar(bar_id, 96);
+            if (et == 0) {
+#pragma unroll
+                for (int pp = 0; pp < GP; ++pp) {
+                    const int64_t v = mt.hdr[pp].x;
+                    if (v < 0) continue;
+                    const int nw = sm.cl_n[b][pp] < lcap ? sm.cl_n[b][pp] : lcap;
+                    const uint32_t bytes = (uint32_t)((16 + 8 * nw + 15) & ~15);
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                                     a.w.clrec + v * (int64_t)CLREC),
+                                 "r"(tc::smem_u32(&sm.rec[b][pp][0])), "r"(bytes)
+                                 : "memory");
+                }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // records reusable
+            }
+#ifdef GRNND_T3_PROF
+            if (lane == 0) T3P_ADD(19, _tx1);
+#endif
+            tc::named_bar(bar_id, 96);  // masks / counters / metadata read: reset for the next groups
             if (et == 0) {
                 sm.qn[b] = 0;
 #pragma unroll
@@ -437,8 +463,9 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             tc::mbar_arrive(&sm.mempty[m]);
         }
     }
+    if ((warp == 2 || warp == 8) && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 #ifdef GRNND_T3_PROF
-    if (lane == 0) T3P_ADD(warp == 0 ? 1 : warp == 1 ? 17 : (warp >= 4 && warp <= 6) ? 8 : warp >= 8 ? 14 : 11, _t3p0);
+    if (lane == 0) T3P_ADD(warp == 0 ? 1 : warp == 1 ? 17 : (warp >= 4 && warp <= 6) ? 8 : warp >= 11 ? 14 : 11, _t3p0);
     if (tid == 0) atomicAdd(&g_t3prof[12], (unsigned long long)nmine);
 #endif
     tc::fence_before();

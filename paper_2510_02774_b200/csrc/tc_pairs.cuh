@@ -125,7 +125,7 @@ template <int SZ>
 struct TcSmem {
     static constexpr int GP = 128 / SZ;  // pools per group
     static constexpr int NM = 4;         // metadata slots
-    static constexpr int CL = 64;        // kept redirect distances per pool
+    static constexpr int CL = PAIR_LIST;  // redirect-capable pairs handed to decide (workspace.cuh)
     static constexpr int QC = 1024;      // filter candidates per group (overflow: exact sweep)
     int32_t ids[NM][128];
     float dv[NM][128];
@@ -276,11 +276,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_pairs_kernel(PropArgs a, int
         const int xa = x1 < x2 ? x1 : x2, xb = x1 < x2 ? x2 : x1;
         const float dva = x1 < x2 ? d1 : d2, dvb = x1 < x2 ? d2 : d1;
         const unsigned long long bit = 1ull << (xb & 63);
+        const bool far = !(dvb >= dva);
         atomicOr((unsigned long long *)&sm.cond[p * SZ + xa][xb >> 6], bit);
-        if (!(dvb >= dva)) atomicOr((unsigned long long *)&sm.afar[p * SZ + xa][xb >> 6], bit);
+        if (far) atomicOr((unsigned long long *)&sm.afar[p * SZ + xa][xb >> 6], bit);
         const int c = atomicAdd(&sm.cl_n[qs][p], 1);
         if (c < S::CL) {
-            sm.cl_key[p][c] = (uint32_t)((xa << 8) | xb);
+            sm.cl_key[p][c] = (uint32_t)((far ? 1u << 16 : 0u) | (xa << 8) | xb);
             sm.cl_d[p][c] = d;
         }
     };
@@ -395,7 +396,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_pairs_kernel(PropArgs a, int
             }
         }
         __syncthreads();  // masks + kept distances complete
-        // ---- masks + kept distances -> global (decide_kernel); masks re-zeroed ----
+        // ---- kept pairs -> global (decide_kernel); masks only for incomplete lists; re-zero ----
+        const int lcap = list_cap(cap);
         for (int e = tid; e < 128 * mw; e += NT) {
             const int r = mw == 2 ? e >> 1 : e, wd = mw == 2 ? e & 1 : 0;  // group row = p * SZ + anchor pos
             const int pp = r / SZ, x = r - pp * SZ;
@@ -408,23 +410,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_pairs_kernel(PropArgs a, int
                 sm.cond[r][wd] = 0ull;
                 sm.afar[r][wd] = 0ull;
             }
-            a.w.cond[(v * cap + x) * mw + wd] = cv;
-            a.w.afar[(v * cap + x) * mw + wd] = fv;
+            if (sm.cl_n[qs][pp] > lcap) {
+                a.w.cond[(v * cap + x) * mw + wd] = cv;
+                a.w.afar[(v * cap + x) * mw + wd] = fv;
+            }
         }
-        const int lcap = S::CL < 4 * cap ? S::CL : 4 * cap;
         for (int e = tid; e < GP * S::CL; e += NT) {
             const int pp = e / S::CL, c = e - pp * S::CL;
             const int64_t v = sm.v[ms][pp];
             if (v < 0) continue;
             const int ncl = sm.cl_n[qs][pp];
             const int nw = ncl < lcap ? ncl : lcap;
+            int32_t *rec = a.w.clrec + v * (int64_t)CLREC;
             if (c == 0) {
-                a.w.cl_n[v] = nw;  // truncated lists: decide re-evaluates misses
+                rec[0] = ncl;
                 red_local += (unsigned long long)ncl;
             }
             if (c < nw) {
-                a.w.cl[v * 4 * (int64_t)cap + c] = sm.cl_key[pp][c];
-                a.w.cl_d[v * 4 * (int64_t)cap + c] = sm.cl_d[pp][c];
+                rec[4 + 2 * c] = (int32_t)sm.cl_key[pp][c];
+                rec[5 + 2 * c] = __float_as_int(sm.cl_d[pp][c]);
             }
         }
     };

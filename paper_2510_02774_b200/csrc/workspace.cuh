@@ -9,6 +9,14 @@ namespace grnnd {
 
 constexpr int NBINS = 8;  // propagate bins by live count k: see propagate.cu
 constexpr int HEAVY_SEG = 32;  // segments longer than this are sorted by a CTA
+// Redirect-capable pairs of a pool, as the pair phase hands them to decide_kernel: one
+// record of CLREC int32 per vertex: [0] = their count, [4 + 2c] = (afar << 16) | (anchor pos
+// << 8) | partner pos and [5 + 2c] = the pair's exact distance (fp32 bits) for c < min(count,
+// list_cap(cap)).  A complete list is all decide needs; only when count > list_cap are the
+// full cond / afar masks written as well.  (16-byte aligned records: bulk-stored by tc3.)
+constexpr int PAIR_LIST = 64;
+constexpr int CLREC = 4 + 2 * PAIR_LIST;
+__host__ __device__ inline int list_cap(int cap) { return PAIR_LIST < 4 * cap ? PAIR_LIST : 4 * cap; }
 
 // small counters block (unsigned long long so atomicAdd works on it)
 enum Counter : int {
@@ -46,9 +54,7 @@ struct Workspace {
     int32_t mw;          // 64-bit words per mask row = ceil(cap / 64)
     uint64_t *cond;      // [n, cap, mw] redirect-condition bits, row = anchor position
     uint64_t *afar;      // [n, cap, mw] "anchor is the farther member" bits
-    int32_t *cl_n;       // [n] redirect-capable pairs found (may exceed the list)
-    uint32_t *cl;        // [n, 4*cap] (key << 16 | ...) packed: key in high 16 bits of the slot
-    float *cl_d;         // [n, 4*cap] their exact distances
+    int32_t *clrec;      // [n, CLREC] redirect-capable pair records (see PAIR_LIST)
     // tensor-core pair phase (tc3_pairs.cuh): group metadata staged contiguously, 96 slots
     // per group (only carved when cap <= 96)
     int32_t *s_ids;
@@ -101,9 +107,7 @@ inline size_t carve(Workspace *w, void *base, int64_t n, int32_t cap, int64_t ms
     t.mw = (cap + 63) / 64 > 0 ? (cap + 63) / 64 : 1;
     t.cond = (uint64_t *)take(8 * N * (size_t)(cap > 0 ? cap : 1) * (size_t)t.mw);
     t.afar = (uint64_t *)take(8 * N * (size_t)(cap > 0 ? cap : 1) * (size_t)t.mw);
-    t.cl_n = (int32_t *)take(4 * N);
-    t.cl = (uint32_t *)take(4 * N * 4 * (size_t)(cap > 0 ? cap : 1));
-    t.cl_d = (float *)take(4 * N * 4 * (size_t)(cap > 0 ? cap : 1));
+    t.clrec = (int32_t *)take(4 * N * (size_t)CLREC);
     const size_t SG = (cap > 0 && cap <= 96) ? N + 8 : 1;  // staging groups (<= one per pool + bins)
     t.s_ids = (int32_t *)take(4 * SG * 96);
     t.s_dv = (float *)take(4 * SG * 96);
