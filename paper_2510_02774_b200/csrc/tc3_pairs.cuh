@@ -199,6 +199,9 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(cv ? 16 : 0));
             }
             if (pi == 0 && lane == 0) T3P_EV(g, 1);
+#ifdef GRNND_T3_PROF
+            if (lane == 0 && blockIdx.x == 0 && g < 64) atomicMax((unsigned long long *)&g_t3trace[g][2], (unsigned long long)clock64());
+#endif
             // one arrive per lane, performed by the hardware when the lane's copies have landed;
             // the MMA thread fences the async proxy before the tensor core reads the stage
             asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&sm.full[s])) : "memory");
@@ -209,6 +212,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             for (int64_t g = 0; g < nmine; ++g) {
                 const int s = (int)(g % NS), m = (int)(g % NM), ac = (int)(g & 1);
                 T3P_WAIT(2, tc::mbar_wait(&sm.full[s], (uint32_t)((g / NS) & 1)));
+                T3P_EV(g, 0);  // (overrides "meta issued"): rows landed, as seen by the MMA thread
                 tc::mbar_wait(&sm.mfull[m], (uint32_t)((g / NM) & 1));
                 T3P_WAIT(3, tc::mbar_wait(&sm.acce[ac], (uint32_t)(((g >> 1) & 1) ^ 1)));
                 tc::fence_after();

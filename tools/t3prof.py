@@ -31,6 +31,6 @@ tr = (C.c_longlong * 512)()
 lib.grnnd_debug_trace(tr)
 t = np.array(list(tr)).reshape(64, 8)
 t0 = t[0, 0]
-print("events (K cycles; CTA 0 of the last bin kernel): 0 meta issued, 1 rows issued, 3 mma issued, 4 filter start, 5 filter done, 6 exact start, 7 exact done")
+print("events (K cycles; CTA 0 of the last bin kernel): 0 meta issued, 1 rows issued (warp 0), 2 rows issued (last warp), 3 mma issued, 4 filter start, 5 filter done, 6 exact start, 7 exact done")
 for gi in range(0, 24):
     print(gi, " ".join(f"{(x - t0) / 1000:8.1f}" for x in t[gi]))

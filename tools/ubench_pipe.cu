@@ -15,6 +15,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     while (!done) asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p; }" : "=r"(done) : "r"(su32(bar)), "r"(parity) : "memory");
 }
 
+__device__ int g_delay;
 template <int NS, int NP, bool NOINC>
 __global__ void k_pipe(const float *__restrict__ data, const int *__restrict__ ids, float *out) {
     extern __shared__ __align__(1024) unsigned char raw[];
@@ -36,6 +37,7 @@ __global__ void k_pipe(const float *__restrict__ data, const int *__restrict__ i
             const int s = g % NS;
             mbar_wait(&full[s], (g / NS) & 1);
             acc += *(float *)(base + s * 49152 + lane * 4);
+            { const long long t0 = clock64(); while (clock64() - t0 < g_delay) { } }
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[s])) : "memory");
         }
@@ -88,6 +90,12 @@ int main() {
         float ms; cudaEventElapsedTime(&ms, e0, e1);
         printf("%-40s %8.3f ms  %7.1f GB/s  %s\n", name, ms, NGROUPS * 96.0 * 512 / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
     };
+    for (int dly : {0, 1000, 2000, 4000, 8000}) {
+        cudaMemcpyToSymbol(g_delay, &dly, 4);
+        char nm[64]; snprintf(nm, 64, "NS=4 NP=9 noinc consumer delay %d", dly);
+        run(nm, k_pipe<4, 9, true>, 10 * 32, 4 * 49152 + 2048);
+    }
+    int z = 0; cudaMemcpyToSymbol(g_delay, &z, 4);
     run("NS=4 NP=12 noinc", k_pipe<4, 12, true>, 13 * 32, 4 * 49152 + 2048);
     run("NS=4 NP=12 waitgroup", k_pipe<4, 12, false>, 13 * 32, 4 * 49152 + 2048);
     run("NS=4 NP=16 noinc", k_pipe<4, 16, true>, 17 * 32, 4 * 49152 + 2048);
