@@ -1,6 +1,7 @@
 #!/bin/bash
-# One GPU-box pass: build check, gpu tests, smoke, bench, ncu launch list, ncu full capture of the
-# dominant kernel.  Outputs under gpurun_out/.
+# One GPU-box pass: gpu tests, smoke, bench (+ reference arm), ncu launch list of the bench
+# command, and an ncu --set full capture of one steady update round's pair-phase kernels
+# (round 21 of a T1=2 T2=15 C2-shape schedule).  Outputs under gpurun_out/<tag>_*.
 cd "$(dirname "$0")/.."
 TAG=${1:-r1}
 mkdir -p gpurun_out
@@ -12,6 +13,9 @@ timeout 600 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/$
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
    python bench.py --no-cpu --steps 1 --warmup 1 > gpurun_out/${TAG}_bench_under_ncu.log 2>&1
 python tools/launch_summary.py gpurun_out/${TAG}_launches.csv > gpurun_out/${TAG}_launch_summary.txt 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"pairs" -s 100 -c 3 \
-   -o gpurun_out/${TAG}_pairs_full -f python tools/prof_rounds.py 1000000 128 2 15 > gpurun_out/${TAG}_ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tc3_pairs|tc_stage|decide" -s 122 -c 7 \
+   -o gpurun_out/${TAG}_round_full -f python tools/prof_rounds.py 1000000 128 2 15 > gpurun_out/${TAG}_ncu_full.log 2>&1
+python tools/ncu_to_json.py gpurun_out/${TAG}_round_full.ncu-rep gpurun_out/${TAG}_pair_phase_ncu.json \
+   "ncu --set full --clock-control none -k regex:tc3_pairs|tc_stage|decide -s 122 -c 7, tools/prof_rounds.py 1000000 128 2 15 (update round 21)" \
+   > gpurun_out/${TAG}_ncu_json.log 2>&1
 echo done
