@@ -195,6 +195,60 @@ __global__ void segsort_light_kernel(const int64_t *__restrict__ starts, int64_t
 
 constexpr int HEAVY_CAP = 8192;
 constexpr int HEAVY_T = 512;
+constexpr int MEDIUM_CAP = 256;  // segments of 33..256 messages: one warp each (rank sort)
+constexpr int MEDIUM_WARPS = 8;
+
+// medium: warp per segment of HEAVY_SEG < len <= MEDIUM_CAP; keys are unique, so each
+// message's rank is the number of smaller keys (keys staged in shared memory)
+__global__ void __launch_bounds__(MEDIUM_WARPS * 32) segsort_medium_kernel(const int64_t *__restrict__ starts,
+                                                                         const int32_t *__restrict__ heavy,
+                                                                         const unsigned long long *__restrict__ heavy_ctr,
+                                                                         int64_t *__restrict__ key, int32_t *__restrict__ id,
+                                                                         float *__restrict__ dist) {
+    __shared__ int64_t sk[MEDIUM_WARPS][MEDIUM_CAP];
+    const int lane = lane_id(), w = threadIdx.x >> 5;
+    const int64_t nh = (int64_t)*heavy_ctr;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t h = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; h < nh; h += warps) {
+        const int64_t t = heavy[h];
+        const int64_t b = starts[t];
+        const int len = (int)(starts[t + 1] - b);
+        if (len > MEDIUM_CAP) continue;  // the CTA kernel takes it
+        constexpr int PER = MEDIUM_CAP / 32;
+        int64_t k[PER];
+        int32_t ii[PER];
+        float dd[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int i = lane + 32 * j;
+            if (i < len) {
+                k[j] = key[b + i];
+                ii[j] = id[b + i];
+                dd[j] = dist[b + i];
+                sk[w][i] = k[j];
+            }
+        }
+        __syncwarp();
+        int r[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) r[j] = 0;
+        for (int t2 = 0; t2 < len; ++t2) {
+            const int64_t kt = sk[w][t2];
+#pragma unroll
+            for (int j = 0; j < PER; ++j) r[j] += kt < k[j] ? 1 : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int i = lane + 32 * j;
+            if (i < len) {
+                key[b + r[j]] = k[j];
+                id[b + r[j]] = ii[j];
+                dist[b + r[j]] = dd[j];
+            }
+        }
+        __syncwarp();
+    }
+}
 
 // heavy: one CTA per long segment; bitonic sort of (key, index) in smem
 __global__ void __launch_bounds__(HEAVY_T) segsort_heavy_kernel(const int64_t *__restrict__ starts,
@@ -213,6 +267,7 @@ __global__ void __launch_bounds__(HEAVY_T) segsort_heavy_kernel(const int64_t *_
         const int64_t t = heavy[h];
         const int64_t b = starts[t];
         const int64_t len = starts[t + 1] - b;
+        if (len <= MEDIUM_CAP) continue;  // sorted by segsort_medium_kernel
         if (len <= HEAVY_CAP) {
             int P = 1;
             while (P < len) P <<= 1;
@@ -295,6 +350,8 @@ int launch_segsort(const Workspace &w, int64_t n, int64_t *key, int32_t *id, flo
         GRNND_CUDA(cudaFuncSetAttribute(segsort_heavy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = true;
     }
+    segsort_medium_kernel<<<sms * 8, MEDIUM_WARPS * 32, 0, st>>>(w.starts, w.heavy, w.ctr + C_HEAVY, key, id, dist);
+    GRNND_TRY(check_launch("segsort_medium"));
     segsort_heavy_kernel<<<sms, HEAVY_T, smem, st>>>(w.starts, w.heavy, w.ctr + C_HEAVY, key, id, dist, w.o_key,
                                                      w.o_id, w.o_dist);
     return check_launch("segsort_heavy");

@@ -58,6 +58,7 @@ __global__ void bin_kernel(const int32_t *__restrict__ read_count, int64_t n, in
                            int order_code, int32_t *__restrict__ msg_tgt, int32_t *__restrict__ msg_id,
                            float *__restrict__ msg_dist, int32_t *__restrict__ msg_cnt, int tc_bins) {
     __shared__ unsigned long long s_sum;
+    extern __shared__ uint8_t fy_scratch[];  // [blockDim.x][cap]
     if (threadIdx.x == 0) s_sum = 0;
     __syncthreads();
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -75,7 +76,8 @@ __global__ void bin_kernel(const int32_t *__restrict__ read_count, int64_t n, in
             w.bins[(int64_t)b * w.n + (int64_t)base + rank] = make_int2((int)v, k);
             if (order_code == 0) {
                 // perm = identity; for i = k-1..1: swap(perm[i], perm[hash4(seed,stream,v,i) % (i+1)])
-                uint8_t perm[GRNND_MAX_CAP];
+                // (per-thread scratch in shared memory, not local memory)
+                uint8_t *perm = fy_scratch + threadIdx.x * cap;
                 for (int i = 0; i < k; ++i) perm[i] = (uint8_t)i;
                 const uint64_t pre = vertex_prefix(seed, stream_id, (uint64_t)(lo + v));
                 for (int i = k - 1; i > 0; --i) {
@@ -600,7 +602,7 @@ int launch_propagate(const PropArgs &a, cudaStream_t st) {
     GRNND_CUDA(cudaMemsetAsync(a.w.ctr + C_BIN0, 0, sizeof(unsigned long long) * NBINS, st));
     const bool tc3 = GRNND_TC && a.norms && a.dim <= 128 && a.cap <= T3_ROWS && a.order_code == 0;
     const int tb = 128;
-    bin_kernel<<<(unsigned)((n + tb - 1) / tb), tb, 0, st>>>(a.read_count, n, a.cap, a.w, a.stats, a.slice_mode,
+    bin_kernel<<<(unsigned)((n + tb - 1) / tb), tb, (size_t)tb * a.cap, st>>>(a.read_count, n, a.cap, a.w, a.stats, a.slice_mode,
                                                             a.read_ids, a.read_dists, a.lo, a.seed, a.stream_id,
                                                             a.order_code, a.msg_tgt, a.msg_id, a.msg_dist,
                                                             a.msg_cnt, tc3 ? 1 : 0);

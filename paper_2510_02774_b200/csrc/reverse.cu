@@ -1,3 +1,4 @@
+#include <algorithm>
 // reverse.cu -- reverse-edge sampling and the self merge, plus init and finalize kernels.
 //
 // References:
@@ -203,9 +204,9 @@ int launch_sample_initial(int64_t n_total, int64_t lo, int64_t rows, int32_t cou
 }
 
 // init_dists: one thread per (vertex, slot); exact sequential distance
-__global__ void init_dists_kernel(const float *__restrict__ data, int32_t dim, int32_t ld, int64_t lo, int64_t rows,
-                                  const int32_t *__restrict__ ids, int32_t ld_ids, int32_t count,
-                                  float *__restrict__ out, int32_t ld_out) {
+__global__ void init_dists_pair_kernel(const float *__restrict__ data, int32_t dim, int32_t ld, int64_t lo,
+                                       int64_t rows, const int32_t *__restrict__ ids, int32_t ld_ids, int32_t count,
+                                       float *__restrict__ out, int32_t ld_out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= rows * count) return;
     const int64_t r = i / count;
@@ -214,12 +215,66 @@ __global__ void init_dists_kernel(const float *__restrict__ data, int32_t dim, i
     out[r * ld_out + s] = exact_sqdist_global(data + (lo + r) * (int64_t)ld, data + (int64_t)j * ld, dim);
 }
 
+// warp per vertex row: the row is staged once in shared memory; lane s < count walks
+// neighbour s's row (16-byte loads, independent addresses) in the reference's sequential
+// order against it
+constexpr int ID_WARPS = 8;
+__global__ void __launch_bounds__(ID_WARPS * 32) init_dists_kernel(const float *__restrict__ data, int32_t dim,
+                                                                  int32_t ld, int64_t lo, int64_t rows,
+                                                                  const int32_t *__restrict__ ids, int32_t ld_ids,
+                                                                  int32_t count, float *__restrict__ out,
+                                                                  int32_t ld_out) {
+    extern __shared__ float4 id_rows[];  // [ID_WARPS][ld / 4]
+    const int lane = lane_id(), w = threadIdx.x >> 5;
+    const int nq = ld >> 2;
+    float4 *mine = id_rows + w * nq;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += warps) {
+        const float4 *a = reinterpret_cast<const float4 *>(data + (lo + r) * (int64_t)ld);
+        for (int q = lane; q < nq; q += 32) mine[q] = a[q];
+        __syncwarp();
+        for (int s0 = 0; s0 < count; s0 += 32) {
+            const int s = s0 + lane;
+            if (s < count) {
+                const int32_t j = ids[r * ld_ids + s];
+                const float4 *b = reinterpret_cast<const float4 *>(data + (int64_t)j * ld);
+                float acc = 0.0f;
+                const int nfull = dim >> 2;
+#pragma unroll 8
+                for (int q = 0; q < nfull; ++q) {
+                    const float4 x = mine[q], y = __ldg(b + q);
+                    acc = exact_step(acc, x.x, y.x);
+                    acc = exact_step(acc, x.y, y.y);
+                    acc = exact_step(acc, x.z, y.z);
+                    acc = exact_step(acc, x.w, y.w);
+                }
+                if (dim & 3) {  // the first dim % 4 columns of the last chunk (padding ignored)
+                    const float4 x = mine[nfull], y = __ldg(b + nfull);
+                    acc = exact_step(acc, x.x, y.x);
+                    if ((dim & 3) > 1) acc = exact_step(acc, x.y, y.y);
+                    if ((dim & 3) > 2) acc = exact_step(acc, x.z, y.z);
+                }
+                out[r * ld_out + s] = acc;
+            }
+        }
+        __syncwarp();
+    }
+}
+
 int launch_init_dists(const float *data, int32_t dim, int32_t ld, int64_t lo, int64_t rows, const int32_t *ids,
                       int32_t ld_ids, int32_t count, float *out, int32_t ld_out, cudaStream_t st) {
-    const int64_t total = rows * count;
-    if (total <= 0) return GRNND_OK;
-    init_dists_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(data, dim, ld, lo, rows, ids, ld_ids, count,
-                                                                       out, ld_out);
+    if (rows <= 0 || count <= 0) return GRNND_OK;
+    if (ld & 3) {  // rows not float4-addressable: thread per pair
+        const int64_t total = rows * count;
+        init_dists_pair_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(data, dim, ld, lo, rows, ids, ld_ids,
+                                                                                count, out, ld_out);
+        return check_launch("init_dists_pair_kernel");
+    }
+    const size_t smem = (size_t)ID_WARPS * ld * 4;
+    if (smem > 48 * 1024) GRNND_CUDA(cudaFuncSetAttribute(init_dists_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t blocks = std::min<int64_t>((rows + ID_WARPS - 1) / ID_WARPS, 148 * 64);
+    init_dists_kernel<<<(unsigned)blocks, ID_WARPS * 32, smem, st>>>(data, dim, ld, lo, rows, ids, ld_ids, count, out,
+                                                                      ld_out);
     return check_launch("init_dists_kernel");
 }
 

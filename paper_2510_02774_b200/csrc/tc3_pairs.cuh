@@ -133,7 +133,11 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             tc::mbar_init(&sm.mempty[m], 96);
         }
         for (int s = 0; s < NS; ++s) {
+#ifdef GRNND_T3_WAITGROUP
+            tc::mbar_init(&sm.full[s], T3_NP);
+#else
             tc::mbar_init(&sm.full[s], T3_NP * 32);
+#endif
             tc::mbar_init(&sm.empty[s], 96);
         }
         for (int b = 0; b < 2; ++b) {
@@ -204,7 +208,15 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
 #endif
             // one arrive per lane, performed by the hardware when the lane's copies have landed;
             // the MMA thread fences the async proxy before the tensor core reads the stage
+#ifdef GRNND_T3_WAITGROUP
+            cp_async_commit();
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            tc::fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&sm.full[s]);
+#else
             asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&sm.full[s])) : "memory");
+#endif
         }
     } else if (warp == 1) {
         // ================= MMA issuer =================
@@ -226,7 +238,9 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const uint64_t desc = tc::sw128_desc(sa + kb * T3_KB + kk * 32);
+#ifndef GRNND_T3_NOMMA
                         tc::mma_tf32(d, desc, desc, idesc, (kb | kk) != 0);
+#endif
                     }
                 T3P_EV(g, 3);
                 tc::mma_commit(&sm.accf[ac]);
