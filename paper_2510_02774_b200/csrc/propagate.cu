@@ -224,8 +224,6 @@ __device__ __forceinline__ void tile_dot(float (&acc)[T * T], const float4 *__re
 }
 
 #include "pairs.cuh"
-#include "tc_pairs.cuh"
-#include "tc3_pairs.cuh"
 
 // ---------------------------------------------------------------------------------
 // 3. decide kernel: anchor-serial rule over the masks, emission, tombstones
@@ -256,6 +254,168 @@ struct DecideSmem {
     uint16_t e_key[DEC_WARPS][CAPM];  // (anchor pos << 8) | partner pos of message j
 };
 
+// The anchor-serial rule of one pool (SURVEY 7 hard part 1), warp-collective: anchors are
+// visited in permutation-position order; an anchor with a live redirect partner emits its
+// partner-far messages in position order up to the first anchor-far partner (which
+// redirects the anchor and ends its row).  masks(x, c, am) gives anchor x's cond / afar
+// words; dist_of(key, found) looks an emitted pair's exact distance up (warp-collective);
+// missing ones are re-evaluated from global rows.  Emits to the message list (or the
+// reference's slices), tombstones read_ids, counts redirects and reference-semantics pairs.
+template <int MW, class MaskFn, class DistFn>
+__device__ __forceinline__ void decide_pool(const PropArgs &a, int k, int64_t v, const int32_t *ids,
+                                            const uint8_t *pos, int16_t *perm, int16_t *e_tgt, int16_t *e_id,
+                                            uint16_t *e_key, MaskFn masks, DistFn dist_of,
+                                            unsigned long long &red_total, unsigned long long &refp_total) {
+    const int lane = lane_id();
+    const int cap = a.cap;
+    const int64_t vg = a.lo + v;
+    for (int s = lane; s < k; s += 32) perm[pos[s]] = (int16_t)s;
+    __syncwarp();
+    uint64_t live[MW];
+#pragma unroll
+    for (int i = 0; i < MW; ++i) {
+        const int x0 = i * 64;
+        const bool l0 = x0 + lane < k && ids[perm[x0 + lane]] != TOMB;
+        const bool l1 = x0 + 32 + lane < k && ids[perm[x0 + 32 + lane]] != TOMB;
+        live[i] = (uint64_t)__ballot_sync(FULL, l0) | ((uint64_t)__ballot_sync(FULL, l1) << 32);
+    }
+    int nm = 0;
+    unsigned long long refp = 0;
+    for (int x0 = 0; x0 < k - 1; x0 += 32) {
+        const int x = x0 + lane;
+        uint64_t c[MW], am[MW];
+        masks(x, c, am);
+        int cur = x0;
+        while (true) {
+            const bool mylive = x < k - 1 && ((live[x >> 6] >> (x & 63)) & 1ull);
+            bool hit = false;
+#pragma unroll
+            for (int i = 0; i < MW; ++i) hit |= (c[i] & live[i]) != 0ull;
+            const unsigned act = __ballot_sync(FULL, x >= cur && mylive && hit);
+            const int xa = act ? x0 + __ffs(act) - 1 : x0 + 32;
+            // live anchors in [cur, xa) have no live redirect partner: they visit every
+            // live partner after them (reference-semantics pair count)
+            if (x >= cur && x < xa && mylive) {
+#pragma unroll
+                for (int i = 0; i < MW; ++i) refp += __popcll(live[i] & bits_above(x, i));
+            }
+            if (!act) break;
+            const int src = xa - x0;
+            int f = k;
+            uint64_t em[MW];
+            if (lane == src) {
+#pragma unroll
+                for (int i = 0; i < MW; ++i) {
+                    const uint64_t m = am[i] & live[i];
+                    if (m && f == k) f = i * 64 + __ffsll((long long)m) - 1;
+                }
+#pragma unroll
+                for (int i = 0; i < MW; ++i) {
+                    em[i] = c[i] & live[i] & ~am[i] & bits_below(f, i);
+                    // partners visited: live, position in (xa, f] (or (xa, k) without a break)
+                    const uint64_t vis = live[i] & bits_above(xa, i) & (f < k ? bits_below(f + 1, i) : ~0ull);
+                    refp += __popcll(vis);
+                }
+            }
+            f = __shfl_sync(FULL, f, src);
+#pragma unroll
+            for (int i = 0; i < MW; ++i) em[i] = __shfl_sync(FULL, em[i], src);
+            // emission records: partner-far messages in position order, then anchor-far
+            const int sa = perm[xa];
+            int base = nm;
+#pragma unroll
+            for (int i = 0; i < MW; ++i) {
+                const uint64_t m = em[i];
+                if (!m) continue;
+                const uint32_t lo_ = (uint32_t)m, hi_ = (uint32_t)(m >> 32);
+                if ((lo_ >> lane) & 1u) {
+                    const int j = base + __popc(lo_ & ((1u << lane) - 1u));
+                    e_tgt[j] = (int16_t)sa;
+                    e_id[j] = perm[i * 64 + lane];
+                    e_key[j] = (uint16_t)((xa << 8) | (i * 64 + lane));
+                }
+                if ((hi_ >> lane) & 1u) {
+                    const int j = base + __popc(lo_) + __popc(hi_ & ((1u << lane) - 1u));
+                    e_tgt[j] = (int16_t)sa;
+                    e_id[j] = perm[i * 64 + 32 + lane];
+                    e_key[j] = (uint16_t)((xa << 8) | (i * 64 + 32 + lane));
+                }
+                base += __popcll(m);
+                live[i] &= ~m;
+            }
+            if (f < k) {
+                if (lane == 0) {
+                    e_tgt[base] = perm[f];
+                    e_id[base] = (int16_t)sa;
+                    e_key[base] = (uint16_t)((xa << 8) | f);
+                }
+                ++base;
+                live[xa >> 6] &= ~(1ull << (xa & 63));
+            }
+            nm = base;
+            cur = xa + 1;
+        }
+    }
+    __syncwarp();
+    refp_total += refp;
+    red_total += (unsigned long long)nm;
+    unsigned long long base = 0;
+    if (!a.slice_mode && nm > 0) {
+        if (lane == 0) base = atomicAdd(&a.w.ctr[C_LIST], (unsigned long long)nm);
+        base = __shfl_sync(FULL, base, 0);
+    }
+    for (int jb = 0; jb < nm; jb += 32) {
+        const int j = jb + lane;
+        const uint32_t mykey = j < nm ? (uint32_t)e_key[j] : 0xFFFFFFFFu;
+        bool found = false;
+        float d = dist_of(mykey, found);
+        if (j >= nm) continue;
+        const int32_t tgt = ids[e_tgt[j]];
+        const int32_t id = ids[e_id[j]];
+        if (!found)  // list truncated (pathological pools): exact re-evaluation from global rows
+            d = exact_sqdist_global(a.data + (int64_t)tgt * a.ld, a.data + (int64_t)id * a.ld, a.dim);
+        if (a.slice_mode) {
+            a.msg_tgt[v * cap + j] = tgt;
+            a.msg_id[v * cap + j] = id;
+            a.msg_dist[v * cap + j] = d;
+        } else {
+            const unsigned long long p = base + (unsigned long long)j;
+            if (p < (unsigned long long)a.w.msg_capacity) {
+                a.w.e_key[p] = vg * cap + j;
+                a.w.e_tgt[p] = tgt;
+                a.w.e_id[p] = id;
+                a.w.e_dist[p] = d;
+            } else {
+                a.w.ctr[C_OVERFLOW] = 1ull;
+            }
+        }
+    }
+    // tombstones (read_ids mutated in place, as the reference does) + survivors
+    int sbase = nm;
+    for (int s0 = 0; s0 < k; s0 += 32) {
+        const int s = s0 + lane;
+        bool alive = false;
+        if (s < k) {
+            const int x = pos[s];
+            alive = (live[x >> 6] >> (x & 63)) & 1ull;
+            if (!alive && ids[s] != TOMB) a.read_ids[v * cap + s] = TOMB;
+            alive = alive && ids[s] != TOMB;
+        }
+        if (a.slice_mode) {  // survivors in slot order after the redirects (:186-191)
+            const unsigned bal = __ballot_sync(FULL, alive);
+            if (alive) {
+                const int o = sbase + __popc(bal & ((1u << lane) - 1));
+                a.msg_tgt[v * cap + o] = (int32_t)vg;
+                a.msg_id[v * cap + o] = ids[s];
+                a.msg_dist[v * cap + o] = a.read_dists[v * cap + s];
+            }
+            sbase += __popc(bal);
+        }
+    }
+    if (a.slice_mode && lane == 0) a.msg_cnt[v] = sbase;
+    __syncwarp();
+}
+
 template <int MW>
 __global__ void __launch_bounds__(DEC_WARPS * 32) decide_kernel(PropArgs a) {
     __shared__ DecideSmem<MW> sm;
@@ -264,28 +424,15 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) decide_kernel(PropArgs a) {
     const int64_t n = a.hi - a.lo;
     const int cap = a.cap;
     int32_t *ids = sm.ids[wib];
-    int16_t *perm = sm.perm[wib];
     uint8_t *pos = sm.pos[wib];
     unsigned long long red_total = 0, refp_total = 0;
 
     for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
         const int k = a.read_count[v];
         if (k < 2) continue;  // no pairs (slice-mode survivors of k <= 1 come from bin_kernel)
-        const int64_t vg = a.lo + v;
         for (int s = lane; s < k; s += 32) {
             ids[s] = a.read_ids[v * cap + s];
-            const uint8_t x = a.w.pos8[v * a.w.pcap + s];
-            pos[s] = x;
-            perm[x] = (int16_t)s;
-        }
-        __syncwarp();
-        uint64_t live[MW];
-#pragma unroll
-        for (int i = 0; i < MW; ++i) {
-            const int x0 = i * 64;
-            const bool l0 = x0 + lane < k && ids[perm[x0 + lane]] != TOMB;
-            const bool l1 = x0 + 32 + lane < k && ids[perm[x0 + 32 + lane]] != TOMB;
-            live[i] = (uint64_t)__ballot_sync(FULL, l0) | ((uint64_t)__ballot_sync(FULL, l1) << 32);
+            pos[s] = a.w.pos8[v * a.w.pcap + s];
         }
         const uint64_t *gc = a.w.cond + v * (int64_t)cap * MW;
         const uint64_t *ga = a.w.afar + v * (int64_t)cap * MW;
@@ -300,11 +447,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) decide_kernel(PropArgs a) {
         if (lane + 32 < ncl) e1 = *reinterpret_cast<const int2 *>(rec + 4 + 2 * (lane + 32));
         const uint32_t key0 = (uint32_t)e0.x, key1 = (uint32_t)e1.x;
         const float cd0 = __int_as_float(e0.y), cd1 = __int_as_float(e1.y);
-        int nm = 0;
-        unsigned long long refp = 0;
-        for (int x0 = 0; x0 < k - 1; x0 += 32) {
-            const int x = x0 + lane;
-            uint64_t c[MW], am[MW];
+        auto masks = [&](int x, uint64_t (&c)[MW], uint64_t (&am)[MW]) {
             if (from_list) {
 #pragma unroll
                 for (int i = 0; i < MW; ++i) c[i] = am[i] = 0ull;
@@ -329,92 +472,9 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) decide_kernel(PropArgs a) {
                     am[i] = x < k - 1 ? ga[x * MW + i] : 0ull;
                 }
             }
-            int cur = x0;
-            while (true) {
-                const bool mylive = x < k - 1 && ((live[x >> 6] >> (x & 63)) & 1ull);
-                bool hit = false;
-#pragma unroll
-                for (int i = 0; i < MW; ++i) hit |= (c[i] & live[i]) != 0ull;
-                const unsigned act = __ballot_sync(FULL, x >= cur && mylive && hit);
-                const int xa = act ? x0 + __ffs(act) - 1 : x0 + 32;
-                // live anchors in [cur, xa) have no live redirect partner: they visit every
-                // live partner after them (reference-semantics pair count)
-                if (x >= cur && x < xa && mylive) {
-#pragma unroll
-                    for (int i = 0; i < MW; ++i) refp += __popcll(live[i] & bits_above(x, i));
-                }
-                if (!act) break;
-                const int src = xa - x0;
-                int f = k;
-                uint64_t em[MW];
-                if (lane == src) {
-#pragma unroll
-                    for (int i = 0; i < MW; ++i) {
-                        const uint64_t m = am[i] & live[i];
-                        if (m && f == k) f = i * 64 + __ffsll((long long)m) - 1;
-                    }
-#pragma unroll
-                    for (int i = 0; i < MW; ++i) {
-                        em[i] = c[i] & live[i] & ~am[i] & bits_below(f, i);
-                        // partners visited: live, position in (xa, f] (or (xa, k) without a break)
-                        const uint64_t vis = live[i] & bits_above(xa, i) & (f < k ? bits_below(f + 1, i) : ~0ull);
-                        refp += __popcll(vis);
-                    }
-                }
-                f = __shfl_sync(FULL, f, src);
-#pragma unroll
-                for (int i = 0; i < MW; ++i) em[i] = __shfl_sync(FULL, em[i], src);
-                // emission records: partner-far messages in position order, then anchor-far
-                const int sa = perm[xa];
-                int base = nm;
-#pragma unroll
-                for (int i = 0; i < MW; ++i) {
-                    const uint64_t m = em[i];
-                    if (!m) continue;
-                    const uint32_t lo_ = (uint32_t)m, hi_ = (uint32_t)(m >> 32);
-                    if ((lo_ >> lane) & 1u) {
-                        const int j = base + __popc(lo_ & ((1u << lane) - 1u));
-                        sm.e_tgt[wib][j] = (int16_t)sa;
-                        sm.e_id[wib][j] = perm[i * 64 + lane];
-                        sm.e_key[wib][j] = (uint16_t)((xa << 8) | (i * 64 + lane));
-                    }
-                    if ((hi_ >> lane) & 1u) {
-                        const int j = base + __popc(lo_) + __popc(hi_ & ((1u << lane) - 1u));
-                        sm.e_tgt[wib][j] = (int16_t)sa;
-                        sm.e_id[wib][j] = perm[i * 64 + 32 + lane];
-                        sm.e_key[wib][j] = (uint16_t)((xa << 8) | (i * 64 + 32 + lane));
-                    }
-                    base += __popcll(m);
-                    live[i] &= ~m;
-                }
-                if (f < k) {
-                    if (lane == 0) {
-                        sm.e_tgt[wib][base] = perm[f];
-                        sm.e_id[wib][base] = (int16_t)sa;
-                        sm.e_key[wib][base] = (uint16_t)((xa << 8) | f);
-                    }
-                    ++base;
-                    live[xa >> 6] &= ~(1ull << (xa & 63));
-                }
-                nm = base;
-                cur = xa + 1;
-            }
-        }
-        __syncwarp();
-        refp_total += refp;
-        red_total += (unsigned long long)nm;
-        // emit: exact distance re-evaluated from L2-resident rows (same arithmetic as the tiles)
-        unsigned long long base = 0;
-        if (!a.slice_mode && nm > 0) {
-            if (lane == 0) base = atomicAdd(&a.w.ctr[C_LIST], (unsigned long long)nm);
-            base = __shfl_sync(FULL, base, 0);
-        }
-        for (int jb = 0; jb < nm; jb += 32) {
-            const int j = jb + lane;
-            const uint32_t mykey = j < nm ? (uint32_t)sm.e_key[wib][j] : 0xFFFFFFFFu;
-            // the pair phase kept every redirect-capable pair's exact distance: warp search
+        };
+        auto dist_of = [&](uint32_t mykey, bool &found) -> float {
             float d = 0.0f;
-            bool found = false;
             for (int t = 0; t < ncl; ++t) {
                 const uint32_t kk = __shfl_sync(FULL, t < 32 ? key0 : key1, t & 31) & 0xFFFFu;
                 const float dd = __shfl_sync(FULL, t < 32 ? cd0 : cd1, t & 31);
@@ -423,51 +483,10 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) decide_kernel(PropArgs a) {
                     found = true;
                 }
             }
-            if (j >= nm) continue;
-            const int32_t tgt = ids[sm.e_tgt[wib][j]];
-            const int32_t id = ids[sm.e_id[wib][j]];
-            if (!found)  // list truncated (pathological pools): exact re-evaluation from L2
-                d = exact_sqdist_global(a.data + (int64_t)tgt * a.ld, a.data + (int64_t)id * a.ld, a.dim);
-            if (a.slice_mode) {
-                a.msg_tgt[v * cap + j] = tgt;
-                a.msg_id[v * cap + j] = id;
-                a.msg_dist[v * cap + j] = d;
-            } else {
-                const unsigned long long p = base + (unsigned long long)j;
-                if (p < (unsigned long long)a.w.msg_capacity) {
-                    a.w.e_key[p] = vg * cap + j;
-                    a.w.e_tgt[p] = tgt;
-                    a.w.e_id[p] = id;
-                    a.w.e_dist[p] = d;
-                } else {
-                    a.w.ctr[C_OVERFLOW] = 1ull;
-                }
-            }
-        }
-        // tombstones (read_ids mutated in place, as the reference does) + survivors
-        int sbase = nm;
-        for (int s0 = 0; s0 < k; s0 += 32) {
-            const int s = s0 + lane;
-            bool alive = false;
-            if (s < k) {
-                const int x = pos[s];
-                alive = (live[x >> 6] >> (x & 63)) & 1ull;
-                if (!alive && ids[s] != TOMB) a.read_ids[v * cap + s] = TOMB;
-                alive = alive && ids[s] != TOMB;
-            }
-            if (a.slice_mode) {  // survivors in slot order after the redirects (:186-191)
-                const unsigned bal = __ballot_sync(FULL, alive);
-                if (alive) {
-                    const int o = sbase + __popc(bal & ((1u << lane) - 1));
-                    a.msg_tgt[v * cap + o] = (int32_t)vg;
-                    a.msg_id[v * cap + o] = ids[s];
-                    a.msg_dist[v * cap + o] = a.read_dists[v * cap + s];
-                }
-                sbase += __popc(bal);
-            }
-        }
-        if (a.slice_mode && lane == 0) a.msg_cnt[v] = sbase;
-        __syncwarp();
+            return d;
+        };
+        decide_pool<MW>(a, k, v, ids, pos, sm.perm[wib], sm.e_tgt[wib], sm.e_id[wib], sm.e_key[wib], masks, dist_of,
+                        red_total, refp_total);
     }
     refp_total = warp_sum(refp_total);
     if (lane == 0 && a.stats) {
@@ -475,6 +494,9 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) decide_kernel(PropArgs a) {
         if (refp_total) atomicAdd((unsigned long long *)&a.stats[GRNND_ST_PAIRS_REF], refp_total);
     }
 }
+
+#include "tc_pairs.cuh"
+#include "tc3_pairs.cuh"
 
 static int sm_count() {
     static int s = 0;
