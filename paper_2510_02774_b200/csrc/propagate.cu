@@ -372,7 +372,11 @@ __device__ __forceinline__ void decide_pool(const PropArgs &a, int k, int64_t v,
         if (j >= nm) continue;
         const int32_t tgt = ids[e_tgt[j]];
         const int32_t id = ids[e_id[j]];
+#ifndef GRNND_DEC_NOREEVAL
         if (!found)  // list truncated (pathological pools): exact re-evaluation from global rows
+#else
+        if (false)   // timing experiment only (results invalid)
+#endif
             d = exact_sqdist_global(a.data + (int64_t)tgt * a.ld, a.data + (int64_t)id * a.ld, a.dim);
         if (a.slice_mode) {
             a.msg_tgt[v * cap + j] = tgt;

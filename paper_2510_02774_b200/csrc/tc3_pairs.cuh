@@ -28,10 +28,19 @@ constexpr int T3_ROWS = 96;
 constexpr int T3_KB = T3_ROWS * 128;  // one 32-dim k-block of a stage (12 KB)
 constexpr int T3_STAGE = 4 * T3_KB;   // 96 rows x 128 fp32 (48 KB)
 constexpr int T3_NS = 4;              // row stages
-constexpr int T3_NM = 6;              // metadata slots
-constexpr int T3_PAD = 4096;          // the M = 128 MMA reads 32 rows past the last k-block
-constexpr int T3_NT = 640;            // 20 warps
-constexpr int T3_NP = 9;              // row-producer warps (11..19)
+#ifndef GRNND_T3_NM
+#define GRNND_T3_NM 6
+#endif
+#ifndef GRNND_T3_PAD
+#define GRNND_T3_PAD 4096
+#endif
+constexpr int T3_NM = GRNND_T3_NM;    // metadata slots
+constexpr int T3_PAD = GRNND_T3_PAD;  // the M = 128 MMA reads 32 rows past the last k-block
+#ifndef GRNND_T3_WARPS
+#define GRNND_T3_WARPS 20
+#endif
+constexpr int T3_NT = 32 * GRNND_T3_WARPS;  // 20 warps
+constexpr int T3_NP = GRNND_T3_WARPS - 11;  // row-producer warps (11..)
 
 struct T3Meta {  // one group's metadata, filled by bulk copies from the staging arrays
     int32_t ids[T3_ROWS];
@@ -93,7 +102,7 @@ __device__ __forceinline__ int64_t tc_group_base(const unsigned long long *ctr, 
 __device__ unsigned long long g_t3prof[32];
 __device__ long long g_t3trace[64][8];  // CTA 0: per group event times (profiling builds)
 #define T3P_BEGIN() const long long _t3p0 = clock64()
-#define T3P_ADD(slot, since) atomicAdd(&g_t3prof[slot], (unsigned long long)(clock64() - (since)))
+#define T3P_ADD(slot, since) atomicAdd(&t3p_sm[slot], (unsigned long long)(clock64() - (since)))  // per-CTA
 #define T3P_EV(g, ev) do { if (blockIdx.x == 0 && (g) < 64) g_t3trace[(g)][(ev)] = clock64(); } while (0)
 #define T3P_WAIT(slot, stmt) do { const long long _w = clock64(); stmt; if (lane == 0) T3P_ADD(slot, _w); } while (0)
 #else
@@ -101,6 +110,18 @@ __device__ long long g_t3trace[64][8];  // CTA 0: per group event times (profili
 #define T3P_ADD(slot, since)
 #define T3P_EV(g, ev)
 #define T3P_WAIT(slot, stmt) stmt
+#endif
+#ifndef GRNND_T3_NOFILTER
+#define GRNND_T3_NOFILTER 0  // timing experiment only (results invalid): the filter queues nothing
+#endif
+#ifndef GRNND_T3_EARLYREL
+#define GRNND_T3_EARLYREL 0
+#endif
+#ifndef GRNND_T3_PF
+#define GRNND_T3_PF 0
+#endif
+#ifndef GRNND_T3_PF_AHEAD
+#define GRNND_T3_PF_AHEAD 0
 #endif
 
 template <int SZ>
@@ -115,6 +136,11 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
     S &sm = *reinterpret_cast<S *>(base + NS * T3_STAGE + T3_PAD);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef GRNND_T3_PROF
+    __shared__ unsigned long long t3p_sm[32];
+    if (tid < 32) t3p_sm[tid] = 0ull;
+    __syncthreads();
+#endif
     const int64_t nbin = (int64_t)a.w.ctr[C_BIN0 + bin];
     const int64_t ngroups = (nbin + GP - 1) / GP;
     const int64_t G = gridDim.x;
@@ -162,11 +188,11 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
     T3P_BEGIN();
     if (warp == 0) {
         // ================= metadata (bulk copies of the staged group) =================
-        if (lane == 0) {
-            for (int64_t g = 0; g < nmine; ++g) {
-                const int m = (int)(g % NM);
+        for (int64_t g = 0; g < nmine; ++g) {
+            const int m = (int)(g % NM);
+            const int64_t e0 = (gbase + blockIdx.x + g * G) * R;  // first staging slot of the group
+            if (lane == 0) {
                 T3P_WAIT(0, tc::mbar_wait(&sm.mempty[m], (uint32_t)(((g / NM) & 1) ^ 1)));
-                const int64_t e0 = (gbase + blockIdx.x + g * G) * R;  // first staging slot of the group
                 T3Meta &mt = sm.meta[m];
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(&sm.mfull[m])),
                              "r"(T3_META_BYTES)
@@ -178,8 +204,25 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 tc::bulk_g2s(mt.hdr, a.w.s_hdr + (e0 / R) * 8, 64, &sm.mfull[m]);
                 T3P_EV(g, 0);
             }
+            __syncwarp();
+#if GRNND_T3_PF
+            // L2 prefetch of the group's vector rows, NM - 2 groups ahead of the producers: the
+            // row gathers then land from L2 and a stage is held for less time
+            const int64_t ep = e0 + (int64_t)(GRNND_T3_PF_AHEAD) * G * R;
+            if (ep < (gbase + ngroups) * R) {
+                for (int r = lane; r < R; r += 32) {
+                    const int32_t id = __ldg(a.w.s_ids + ep + r);
+                    if (id == TOMB) continue;
+                    const float *src = a.data + (int64_t)id * a.ld;
+#if GRNND_T3_PF == 1
+                    for (int c = 0; c < nq * 16; c += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"((const char *)src + c));
+#else
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(nq * 16) : "memory");
+#endif
+                }
+            }
+#endif
         }
-        __syncwarp();
     } else if (warp >= 11) {
         // ================= row producers (9 warps) =================
         // warp pi stages group rows pi, pi + 9, ..: one 512-byte row per instruction (lane =
@@ -227,8 +270,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 T3P_EV(g, 0);  // (overrides "meta issued"): rows landed, as seen by the MMA thread
                 tc::mbar_wait(&sm.mfull[m], (uint32_t)((g / NM) & 1));
                 T3P_WAIT(3, tc::mbar_wait(&sm.acce[ac], (uint32_t)(((g >> 1) & 1) ^ 1)));
-                tc::fence_after();
-                tc::fence_proxy_async();  // cp.async (generic proxy) writes -> tensor core reads
+                T3P_WAIT(20, tc::fence_after(); tc::fence_proxy_async());  // cp.async (generic proxy) writes -> tensor core reads
                 const int n = GP == 1 ? ((sm.meta[m].hdr[0].y + 15) / 16 * 16) : R;
                 const uint32_t idesc = tc::idesc_tf32(n < 16 ? 16 : n);
                 const uint32_t sa = tc::smem_u32(base + s * T3_STAGE);
@@ -243,7 +285,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
 #endif
                     }
                 T3P_EV(g, 3);
-                tc::mma_commit(&sm.accf[ac]);
+                T3P_WAIT(21, tc::mma_commit(&sm.accf[ac]));
             }
         }
         __syncwarp();
@@ -263,11 +305,16 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 if (!(nr <= 1.0e37f)) A = -INFINITY;  // rearranged test could overflow: always a candidate
                 sm.ab[b][i] = live ? make_float2(A, fmaf(mt.dv[i], 1.0f + eps_h, 1e-30f)) : make_float2(0.0f, -1.0f);
             }
-            T3P_WAIT(5, tc::named_bar(1, 96));
+            // queue b free (the exact set of group g - 2 has read it): reset its count
             T3P_WAIT(6, tc::mbar_wait(&sm.qemp[b], (uint32_t)(((g >> 1) & 1) ^ 1)));
+            if (tid == 128) sm.qn[b] = 0;
+            T3P_WAIT(5, tc::named_bar(1, 96));
             T3P_WAIT(7, tc::mbar_wait(&sm.accf[b], (uint32_t)((g >> 1) & 1)));
             if (tid == 128) T3P_EV(g, 4);
             tc::fence_after();
+#if GRNND_T3_EARLYREL == 2  // timing experiment only (results invalid): release at MMA completion
+            tc::mbar_arrive(&sm.empty[(int)(g % NS)]);
+#endif
             const float2 abi = sm.ab[b][i];
             const int kcols = GP == 1 ? mt.hdr[0].y : R;
             const uint32_t trow = tmem + ((uint32_t)(fw * 32) << 16) + (uint32_t)(b * 128);
@@ -306,7 +353,8 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                     }
                 }
             };
-            if (GP == 1) {
+            if (GRNND_T3_NOFILTER) {
+            } else if (GP == 1) {
                 // upper-triangle 32x32 blocks (a, b'), a <= b' < 3, two per warp: (fw, fw) and
                 // (fw, fw+1); warp 2 takes (0, 2) as its transpose (rows 64.., columns 0..31)
                 const int c0 = fw * 32, c1 = fw < 2 ? fw * 32 + 32 : 0;
@@ -362,6 +410,9 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             const unsigned char *stg = base + s * T3_STAGE;
             const T3Meta &mt = sm.meta[m];
             T3P_WAIT(9, tc::mbar_wait(&sm.qrdy[b], (uint32_t)((g >> 1) & 1)));
+#if GRNND_T3_EARLYREL == 1  // timing experiment only (results invalid): release at filter completion
+            tc::mbar_arrive(&sm.empty[s]);
+#endif
             auto record = [&](int i, int j, float d) {  // pair of group rows i < j, same pool
                 const int p = i / SZ;
                 const int x1 = mt.pos[i], x2 = mt.pos[j];
@@ -378,7 +429,16 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                     sm.rec[b][p][5 + 2 * c] = __float_as_int(d);
                 }
             };
+            // this thread's queue entries to registers, then hand the queue back to the filter
             const int qn = sm.qn[b];
+            constexpr int QT = (S::QC + NE - 1) / NE;
+            uint32_t qk[QT + (QT & 1)];
+#pragma unroll
+            for (int t = 0; t < QT + (QT & 1); ++t) {
+                const int e = et + NE * t;
+                qk[t] = (qn <= S::QC && e < qn) ? sm.q[b][e] : 0u;
+            }
+            tc::mbar_arrive(&sm.qemp[b]);
             if (et == 0) T3P_EV(g, 6);
 #ifdef GRNND_T3_PROF
             const long long _tx0 = clock64();
@@ -388,9 +448,12 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 st_ovf += qn > S::QC ? 1ull : 0ull;
             }
             if (qn <= S::QC) {
-                for (int e = et; e < qn; e += 2 * NE) {
+#pragma unroll
+                for (int t = 0; t < QT; t += 2) {
+                    const int e = et + NE * t;
+                    if (e >= qn) break;
                     const bool two = e + NE < qn;
-                    const uint32_t k1 = sm.q[b][e], k2 = two ? sm.q[b][e + NE] : k1;
+                    const uint32_t k1 = qk[t], k2 = two ? qk[t + 1] : k1;
                     const int i1 = (int)(k1 >> 8), j1 = (int)(k1 & 255u), i2 = (int)(k2 >> 8), j2 = (int)(k2 & 255u);
                     float x1, x2;
                     exact2(stg, i1, j1, i2, j2, x1, x2);
@@ -430,7 +493,9 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             const long long _tx1 = clock64();
 #endif
             // the stage's rows are no longer read: let the producers refill it
+#if !GRNND_T3_EARLYREL
             tc::mbar_arrive(&sm.empty[s]);
+#endif
             // pair records -> global by bulk stores (decide_kernel); masks only for incomplete
             // lists (rare; regular stores); every mask row re-zeroed for the next group
             const int lcap = list_cap(cap);
@@ -472,22 +537,23 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
 #endif
             tc::named_bar(bar_id, 96);  // masks / counters / metadata read: reset for the next groups
             if (et == 0) {
-                sm.qn[b] = 0;
 #pragma unroll
                 for (int p = 0; p < GP; ++p) sm.cl_n[b][p] = 0;
             }
             if (et == 0) T3P_EV(g, 7);
-            tc::mbar_arrive(&sm.qemp[b]);
             tc::mbar_arrive(&sm.mempty[m]);
         }
     }
     if ((warp == 2 || warp == 8) && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 #ifdef GRNND_T3_PROF
     if (lane == 0) T3P_ADD(warp == 0 ? 1 : warp == 1 ? 17 : (warp >= 4 && warp <= 6) ? 8 : warp >= 11 ? 14 : 11, _t3p0);
-    if (tid == 0) atomicAdd(&g_t3prof[12], (unsigned long long)nmine);
+    if (tid == 0) atomicAdd(&t3p_sm[12], (unsigned long long)nmine);
 #endif
     tc::fence_before();
     __syncthreads();
+#ifdef GRNND_T3_PROF
+    if (tid < 32 && t3p_sm[tid]) atomicAdd(&g_t3prof[tid], t3p_sm[tid]);
+#endif
     if (warp == 1) tc::tmem_dealloc(tmem, TC_TMEM_COLS);
     if (a.stats) {
         st_pairs = warp_sum(st_pairs);

@@ -15,7 +15,7 @@ row = torch.zeros(16, dtype=torch.int64, device="cuda")
 buf = (C.c_ulonglong * 32)()
 # slot, name, number of timed warps (lane 0 of each)
 rows = [(0, "meta wait mempty", 1), (1, "meta total", 1), (2, "mma wait full", 1), (3, "mma wait acce", 1),
-        (17, "mma total", 1), (4, "filt wait mfull", 3), (5, "filt bar1", 3), (6, "filt wait qemp", 3),
+        (17, "mma total", 1), (20, "mma fence", 1), (21, "mma commit", 1), (4, "filt wait mfull", 3), (5, "filt bar1", 3), (6, "filt wait qemp", 3),
         (7, "filt wait accf", 3), (8, "filt total", 3), (9, "exact wait qrdy", 3), (10, "exact bar2", 3),
         (11, "exact total", 6), (18, "exact chains", 3), (19, "exact write-out", 3), (15, "rows wait mfull", 9), (16, "rows wait empty", 9), (14, "rows total", 9)]
 for r in range(25):
