@@ -32,10 +32,16 @@ constexpr int T3_NS = 4;              // row stages
 #define GRNND_T3_NM 6
 #endif
 #ifndef GRNND_T3_PAD
-#define GRNND_T3_PAD 4096
+#define GRNND_T3_PAD 0
 #endif
+#ifndef GRNND_T3_WCOOP
+#define GRNND_T3_WCOOP 24
+#endif
+constexpr int T3_WCOOP = GRNND_T3_WCOOP;  // queues up to this length: warp-cooperative chains (<= 32)
 constexpr int T3_NM = GRNND_T3_NM;    // metadata slots
-constexpr int T3_PAD = GRNND_T3_PAD;  // the M = 128 MMA reads 32 rows past the last k-block
+// the M = 128 MMA reads 32 rows (4 KB) past the last k-block of the last stage: with no pad
+// those are bytes of T3Smem (> 4 KB), read into accumulator rows 96..127 that nothing uses
+constexpr int T3_PAD = GRNND_T3_PAD;
 #ifndef GRNND_T3_WARPS
 #define GRNND_T3_WARPS 20
 #endif
@@ -64,6 +70,7 @@ struct T3Smem {
     int cl_n[2][GP];
     int qn[2];
     uint32_t q[2][QC];            // (row i << 8) | row j
+    alignas(16) float psq[6][2][128];  // per exact warp: the squared differences of two pairs
     uint64_t mfull[T3_NM], mempty[T3_NM], full[T3_NS], empty[T3_NS], accf[2], acce[2], qrdy[2], qemp[2];
     uint32_t tmem_base;
 };
@@ -110,6 +117,9 @@ __device__ long long g_t3trace[64][8];  // CTA 0: per group event times (profili
 #define T3P_ADD(slot, since)
 #define T3P_EV(g, ev)
 #define T3P_WAIT(slot, stmt) stmt
+#endif
+#ifndef GRNND_T3_BULKREC
+#define GRNND_T3_BULKREC 1  // pair records written by bulk stores (TMA); 0: st.global (measured slower)
 #endif
 #ifndef GRNND_T3_NOFILTER
 #define GRNND_T3_NOFILTER 0  // timing experiment only (results invalid): the filter queues nothing
@@ -431,6 +441,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             };
             // this thread's queue entries to registers, then hand the queue back to the filter
             const int qn = sm.qn[b];
+            const uint32_t qw = (qn <= 32 && lane < qn) ? sm.q[b][lane] : 0u;  // short queues: per warp
             constexpr int QT = (S::QC + NE - 1) / NE;
             uint32_t qk[QT + (QT & 1)];
 #pragma unroll
@@ -447,7 +458,50 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 st_cand += (unsigned long long)qn;
                 st_ovf += qn > S::QC ? 1ull : 0ull;
             }
-            if (qn <= S::QC) {
+            if (qn <= T3_WCOOP) {
+                // short queue: a warp per two pairs: the lanes square 16-byte chunks of the rows in
+                // parallel (one shared-memory latency instead of one per chunk) into a scratch
+                // row, then lanes 0 / 1 sum the squares in the reference's order
+                const int ew = et >> 5;
+                for (int e = ew; e < qn; e += 6) {  // warp-uniform
+                    const bool two = e + 3 < qn;
+                    const uint32_t k1 = __shfl_sync(FULL, qw, e), k2 = __shfl_sync(FULL, qw, two ? e + 3 : e);
+                    const int i1 = (int)(k1 >> 8), j1 = (int)(k1 & 255u), i2 = (int)(k2 >> 8), j2 = (int)(k2 & 255u);
+                    float4 p1 = make_float4(0.f, 0.f, 0.f, 0.f), p2 = p1;
+                    if (lane < nq) {
+                        const float4 x1 = *reinterpret_cast<const float4 *>(stg + t3_off(i1, lane));
+                        const float4 y1 = *reinterpret_cast<const float4 *>(stg + t3_off(j1, lane));
+                        const float4 x2 = *reinterpret_cast<const float4 *>(stg + t3_off(i2, lane));
+                        const float4 y2 = *reinterpret_cast<const float4 *>(stg + t3_off(j2, lane));
+                        p1 = make_float4(exact_step(0.f, x1.x, y1.x), exact_step(0.f, x1.y, y1.y), exact_step(0.f, x1.z, y1.z),
+                                         exact_step(0.f, x1.w, y1.w));
+                        p2 = make_float4(exact_step(0.f, x2.x, y2.x), exact_step(0.f, x2.y, y2.y), exact_step(0.f, x2.z, y2.z),
+                                         exact_step(0.f, x2.w, y2.w));
+                    }
+                    {
+                        float *ps = &sm.psq[E * 3 + ew][0][0];
+                        reinterpret_cast<float4 *>(ps)[lane] = p1;
+                        reinterpret_cast<float4 *>(ps + 128)[lane] = p2;
+                        __syncwarp();
+                        if (lane < 2) {  // lane 0: pair 1, lane 1: pair 2; the reference's order
+                            const float4 *pv = reinterpret_cast<const float4 *>(ps + 128 * lane);
+                            float sx = 0.0f;
+#pragma unroll 8
+                            for (int c = 0; c < nq; ++c) {
+                                const float4 v = pv[c];
+                                sx = __fadd_rn(sx, v.x);
+                                sx = __fadd_rn(sx, v.y);
+                                sx = __fadd_rn(sx, v.z);
+                                sx = __fadd_rn(sx, v.w);
+                            }
+                            const int ii = lane ? i2 : i1, jj = lane ? j2 : j1;
+                            const float av = mt.dv[ii], bv = mt.dv[jj];
+                            if ((lane == 0 || two) && sx < (av >= bv ? av : bv)) record(ii, jj, sx);
+                        }
+                        __syncwarp();
+                    }
+                }
+            } else if (qn <= S::QC) {
 #pragma unroll
                 for (int t = 0; t < QT; t += 2) {
                     const int e = et + NE * t;
@@ -496,7 +550,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
 #if !GRNND_T3_EARLYREL
             tc::mbar_arrive(&sm.empty[s]);
 #endif
-            // pair records -> global by bulk stores (decide_kernel); masks only for incomplete
+            // pair records -> global (decide_kernel); masks only for incomplete
             // lists (rare; regular stores); every mask row re-zeroed for the next group
             const int lcap = list_cap(cap);
             if (et < GP && mt.hdr[et].x >= 0) {
@@ -515,8 +569,8 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                     a.w.afar[(v * cap + x) * mw + wd] = fv;
                 }
             }
-            tc::fence_proxy_async();  // record stores (generic proxy) -> bulk-store reads (async proxy)
-            tc::named_bar(bar_id, 96);
+            tc::named_bar(bar_id, 96);  // record headers written
+#if GRNND_T3_BULKREC
             if (et == 0) {
 #pragma unroll
                 for (int pp = 0; pp < GP; ++pp) {
@@ -524,6 +578,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                     if (v < 0) continue;
                     const int nw = sm.cl_n[b][pp] < lcap ? sm.cl_n[b][pp] : lcap;
                     const uint32_t bytes = (uint32_t)((16 + 8 * nw + 15) & ~15);
+                    tc::fence_proxy_async();
                     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
                                      a.w.clrec + v * (int64_t)CLREC),
                                  "r"(tc::smem_u32(&sm.rec[b][pp][0])), "r"(bytes)
@@ -532,6 +587,18 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // records reusable
             }
+#else
+            // pair records -> global (8-byte stores by the whole set; no async-proxy round trip)
+#pragma unroll
+            for (int pp = 0; pp < GP; ++pp) {
+                const int64_t v = mt.hdr[pp].x;
+                if (v < 0) continue;
+                const int nw = sm.cl_n[b][pp] < lcap ? sm.cl_n[b][pp] : lcap;
+                int2 *dst = reinterpret_cast<int2 *>(a.w.clrec + v * (int64_t)CLREC);
+                const int2 *src = reinterpret_cast<const int2 *>(&sm.rec[b][pp][0]);
+                for (int w = et; w < 2 + nw; w += NE) dst[w] = src[w];
+            }
+#endif
 #ifdef GRNND_T3_PROF
             if (lane == 0) T3P_ADD(19, _tx1);
 #endif
@@ -544,7 +611,9 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             tc::mbar_arrive(&sm.mempty[m]);
         }
     }
+#if GRNND_T3_BULKREC
     if ((warp == 2 || warp == 8) && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#endif
 #ifdef GRNND_T3_PROF
     if (lane == 0) T3P_ADD(warp == 0 ? 1 : warp == 1 ? 17 : (warp >= 4 && warp <= 6) ? 8 : warp >= 11 ? 14 : 11, _t3p0);
     if (tid == 0) atomicAdd(&t3p_sm[12], (unsigned long long)nmine);

@@ -12,5 +12,6 @@ while [ $# -ge 2 ]; do
   done
   wait
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libgrnnd_b200.so $out/obj/*.o -lcudart
+  rm -rf $out/obj
   echo built $out
 done
