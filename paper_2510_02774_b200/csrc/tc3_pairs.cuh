@@ -64,6 +64,7 @@ struct T3Smem {
     static constexpr int QC = 512;   // filter candidates per group (overflow: exact sweep)
     T3Meta meta[T3_NM];
     float2 ab[2][T3_ROWS];        // filter terms (A = -inf: always a candidate; B = -1: dead row)
+    uint32_t livec[2][4];         // bit r: row r's B >= 0 (a column that can pair)
     uint64_t cond[2][T3_ROWS][2];  // per exact set: row = p * SZ + anchor position; bit = partner
     uint64_t afar[2][T3_ROWS][2];
     alignas(16) int32_t rec[2][GP][CLREC];  // per exact set, per pool: pair records (workspace.cuh)
@@ -307,14 +308,23 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             const int m = (int)(g % NM), b = (int)(g & 1);
             T3P_WAIT(4, tc::mbar_wait(&sm.mfull[m], (uint32_t)((g / NM) & 1)));
             const T3Meta &mt = sm.meta[m];
+#ifdef GRNND_T3_PROF
+            const long long _tf0 = clock64();
+#endif
             {  // this row's filter terms
                 const int p = i / SZ, sl = i - p * SZ;
                 const bool live = sl < mt.hdr[p].y && mt.ids[i] != TOMB;
                 const float nr = mt.nrm[i];
                 float A = nr * (1.0f - TC_EPS);
                 if (!(nr <= 1.0e37f)) A = -INFINITY;  // rearranged test could overflow: always a candidate
-                sm.ab[b][i] = live ? make_float2(A, fmaf(mt.dv[i], 1.0f + eps_h, 1e-30f)) : make_float2(0.0f, -1.0f);
+                const float2 t = live ? make_float2(A, fmaf(mt.dv[i], 1.0f + eps_h, 1e-30f)) : make_float2(0.0f, -1.0f);
+                sm.ab[b][i] = t;
+                const unsigned ok = __ballot_sync(FULL, t.y >= 0.0f);
+                if (lane == 0) sm.livec[b][fw] = ok;
             }
+#ifdef GRNND_T3_PROF
+            if (lane == 0) T3P_ADD(22, _tf0);
+#endif
             // queue b free (the exact set of group g - 2 has read it): reset its count
             T3P_WAIT(6, tc::mbar_wait(&sm.qemp[b], (uint32_t)(((g >> 1) & 1) ^ 1)));
             if (tid == 128) sm.qn[b] = 0;
@@ -322,8 +332,19 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             T3P_WAIT(7, tc::mbar_wait(&sm.accf[b], (uint32_t)((g >> 1) & 1)));
             if (tid == 128) T3P_EV(g, 4);
             tc::fence_after();
+#ifdef GRNND_T3_PROF
+            const long long _tf1 = clock64();
+#endif
 #if GRNND_T3_EARLYREL == 2  // timing experiment only (results invalid): release at MMA completion
             tc::mbar_arrive(&sm.empty[(int)(g % NS)]);
+#endif
+#ifdef GRNND_T3_PROF
+            {  // shared-memory load latency as seen by the filter
+                const long long _l0 = clock64();
+                const float v = *(volatile float *)&sm.ab[b][i].x;
+                if (__float_as_uint(v) == 0x7fc00001u) sm.qn[b] = 0;  // never: consumes v
+                if (lane == 0) T3P_ADD(24, _l0);
+            }
 #endif
             const float2 abi = sm.ab[b][i];
             const int kcols = GP == 1 ? mt.hdr[0].y : R;
@@ -331,26 +352,36 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             unsigned np = 0;
             // 16 Gram columns [cb, cb+16) of this warp's rows; tr: the columns are the smaller
             // member of each pair (a block below the diagonal read in place of its transpose)
-            auto scan16 = [&](int cb, bool tr) {
-                uint32_t r[16];
-                tc::tmem_ld16(trow + (uint32_t)cb, r);
+            auto scan16 = [&](const uint32_t *r, int cb, bool tr) {
                 float4 ab4[8];  // column terms, two columns per 16-byte load
 #pragma unroll
                 for (int c = 0; c < 8; ++c) ab4[c] = *reinterpret_cast<const float4 *>(&sm.ab[b][cb + 2 * c]);
+                // pairs of this row with columns cb..cb+15 that can be tested: live column, the
+                // right side of the diagonal, the same pool, live row (bit masks, not per column)
+                uint32_t vm = (sm.livec[b][cb >> 5] >> (cb & 16)) & 0xFFFFu;
+                {
+                    const int d = i - cb;
+                    vm &= tr ? (d <= 0 ? 0u : d >= 16 ? 0xFFFFu : (1u << d) - 1u)
+                             : (d < 0 ? 0xFFFFu : d >= 15 ? 0u : (0xFFFFu << (d + 1)) & 0xFFFFu);
+                    if (GP > 1) {
+                        const int lo = (i / SZ) * SZ - cb, hi = lo + SZ;  // columns [lo, hi) of this pool
+                        vm &= (lo <= 0 ? 0xFFFFu : lo >= 16 ? 0u : (0xFFFFu << lo) & 0xFFFFu) &
+                              (hi >= 16 ? 0xFFFFu : hi <= 0 ? 0u : (1u << hi) - 1u);
+                    }
+                    if (!(abi.y >= 0.0f)) vm = 0u;
+                }
+                np += (unsigned)__popc(vm);
                 uint32_t cm = 0u;
 #pragma unroll
                 for (int c = 0; c < 16; ++c) {
-                    const int jr = cb + c;
                     const float ax = (c & 1) ? ab4[c >> 1].z : ab4[c >> 1].x;
                     const float ay = (c & 1) ? ab4[c >> 1].w : ab4[c >> 1].y;
-                    const bool valid = (tr ? jr < i : jr > i) && (GP == 1 || (jr / SZ) == (i / SZ)) && ay >= 0.0f &&
-                                       abi.y >= 0.0f;
-                    np += valid ? 1u : 0u;
                     // settled iff (|a|^2+|b|^2)(1-eps) - 2G >= max(dv)(1+eps_h) + tiny (tc_pairs.cuh)
                     const float lhs = fmaf(-2.0f, __uint_as_float(r[c]), abi.x + ax);
                     const float rhs = abi.y >= ay ? abi.y : ay;
-                    cm |= (valid && !(lhs >= rhs)) ? (1u << c) : 0u;
+                    cm |= !(lhs >= rhs) ? (1u << c) : 0u;
                 }
+                cm &= vm;
                 if (__any_sync(FULL, cm != 0u)) {
                     const int n = __popc(cm);
                     int qi = n ? atomicAdd(&sm.qn[b], n) : 0;
@@ -363,6 +394,14 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                     }
                 }
             };
+            // Gram columns in 32-column TMEM loads
+            auto scan32 = [&](int cb, int hi, bool tr) {  // columns [cb, min(cb + 32, hi))
+                uint32_t r[32];
+                tc::tmem_ld32_nw(trow + (uint32_t)cb, r);
+                tc::tmem_wait_ld();
+                scan16(r, cb, tr);
+                if (cb + 16 < hi) scan16(r + 16, cb + 16, tr);
+            };
             if (GRNND_T3_NOFILTER) {
             } else if (GP == 1) {
                 // upper-triangle 32x32 blocks (a, b'), a <= b' < 3, two per warp: (fw, fw) and
@@ -370,18 +409,20 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 const int c0 = fw * 32, c1 = fw < 2 ? fw * 32 + 32 : 0;
                 const bool t1 = fw == 2;
 #pragma unroll 1
-                for (int h = 0; h < 4; ++h) {  // warp-uniform
-                    const int cb = (h < 2 ? c0 : c1) + (h & 1) * 16;
-                    if (cb >= kcols) continue;
-                    scan16(cb, h >= 2 && t1);
+                for (int h = 0; h < 2; ++h) {  // warp-uniform
+                    const int cb = h ? c1 : c0;
+                    if (cb < kcols) scan32(cb, kcols, h && t1);
                 }
             } else {
                 const int c_lo = ((fw * 32) / SZ) * SZ, c_hi = ((fw * 32 + 31) / SZ + 1) * SZ;
                 const int start = ((c_lo >> 4) << 4) > fw * 32 ? ((c_lo >> 4) << 4) : fw * 32;
 #pragma unroll 1
-                for (int cb = start; cb < c_hi; cb += 16) scan16(cb, false);  // warp-uniform
+                for (int cb = start; cb < c_hi; cb += 32) scan32(cb, c_hi, false);  // warp-uniform
             }
             st_pairs += np;
+#ifdef GRNND_T3_PROF
+            if (lane == 0) T3P_ADD(23, _tf1);
+#endif
             tc::fence_before();
             if (tid == 128) T3P_EV(g, 5);
             tc::mbar_arrive(&sm.acce[b]);

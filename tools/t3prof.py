@@ -16,7 +16,7 @@ buf = (C.c_ulonglong * 32)()
 # slot, name, number of timed warps (lane 0 of each)
 rows = [(0, "meta wait mempty", 1), (1, "meta total", 1), (2, "mma wait full", 1), (3, "mma wait acce", 1),
         (17, "mma total", 1), (20, "mma fence", 1), (21, "mma commit", 1), (4, "filt wait mfull", 3), (5, "filt bar1", 3), (6, "filt wait qemp", 3),
-        (7, "filt wait accf", 3), (8, "filt total", 3), (9, "exact wait qrdy", 3), (10, "exact bar2", 3),
+        (7, "filt wait accf", 3), (22, "filt ab terms", 3), (23, "filt scan", 3), (24, "filt one LDS", 3), (8, "filt total", 3), (9, "exact wait qrdy", 3), (10, "exact bar2", 3),
         (11, "exact total", 6), (18, "exact chains", 3), (19, "exact write-out", 3), (15, "rows wait mfull", 9), (16, "rows wait empty", 9), (14, "rows total", 9)]
 for r in range(25):
     st.pools.update(p.seed, 1 + st.round_index, 0, row); st.round_index += 1
