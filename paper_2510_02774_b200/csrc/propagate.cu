@@ -681,9 +681,9 @@ extern "C" int grnnd_debug_counters(unsigned long long *out, int n) {
     if (cudaMemcpyToSymbol(grnnd::g_t3prof, z, sizeof(z)) != cudaSuccess) return GRNND_ECUDA;
     return GRNND_OK;
 }
-extern "C" int grnnd_debug_trace(long long *out) {  // 64 x 8 event clocks of CTA 0 (read + reset)
-    if (cudaMemcpyFromSymbol(out, grnnd::g_t3trace, sizeof(long long) * 512) != cudaSuccess) return GRNND_ECUDA;
-    static long long z[512] = {0};
+extern "C" int grnnd_debug_trace(long long *out) {  // 64 x 10 event clocks of CTA 0 (read + reset)
+    if (cudaMemcpyFromSymbol(out, grnnd::g_t3trace, sizeof(long long) * 640) != cudaSuccess) return GRNND_ECUDA;
+    static long long z[640] = {0};
     if (cudaMemcpyToSymbol(grnnd::g_t3trace, z, sizeof(z)) != cudaSuccess) return GRNND_ECUDA;
     return GRNND_OK;
 }

@@ -45,8 +45,16 @@ constexpr int T3_PAD = GRNND_T3_PAD;
 #ifndef GRNND_T3_WARPS
 #define GRNND_T3_WARPS 20
 #endif
-constexpr int T3_NT = 32 * GRNND_T3_WARPS;  // 20 warps
-constexpr int T3_NP = GRNND_T3_WARPS - 11;  // row-producer warps (11..)
+#ifndef GRNND_T3_FSPLIT
+#define GRNND_T3_FSPLIT 0  // 1: warps 20..22 take half of the filter's Gram columns (23 warps)
+#endif
+constexpr int T3_NT = 32 * GRNND_T3_WARPS;
+#ifndef GRNND_T3_STOREW
+#define GRNND_T3_STOREW 0  // 1: the last warp issues the pair-record bulk stores for the exact sets
+#endif
+constexpr int T3_NP = GRNND_T3_WARPS - 11 - 3 * GRNND_T3_FSPLIT - GRNND_T3_STOREW;  // row producers (11..)
+constexpr int T3_NF = 96 * (1 + GRNND_T3_FSPLIT);                  // filter threads
+static_assert(!GRNND_T3_FSPLIT || (11 + T3_NP) % 4 == 0, "filter warps must map to TMEM lane quarters 0..2");
 
 struct T3Meta {  // one group's metadata, filled by bulk copies from the staging arrays
     int32_t ids[T3_ROWS];
@@ -73,12 +81,18 @@ struct T3Smem {
     uint32_t q[2][QC];            // (row i << 8) | row j
     alignas(16) float psq[6][2][128];  // per exact warp: the squared differences of two pairs
     uint64_t mfull[T3_NM], mempty[T3_NM], full[T3_NS], empty[T3_NS], accf[2], acce[2], qrdy[2], qemp[2];
+    uint64_t recrdy[2], recfree[2];  // records of a group complete / read by the bulk stores (STOREW)
     uint32_t tmem_base;
 };
 
 namespace tc {
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// one arrival per warp, after every lane's prior shared-memory accesses (barrier counts = warps)
+__device__ __forceinline__ void warp_arrive(uint64_t *bar) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
 }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
@@ -108,25 +122,24 @@ __device__ __forceinline__ int64_t tc_group_base(const unsigned long long *ctr, 
 
 #ifdef GRNND_T3_PROF
 __device__ unsigned long long g_t3prof[32];
-__device__ long long g_t3trace[64][8];  // CTA 0: per group event times (profiling builds)
+__device__ long long g_t3trace[64][10];  // CTA 0: per group event times (profiling builds)
 #define T3P_BEGIN() const long long _t3p0 = clock64()
-#define T3P_ADD(slot, since) atomicAdd(&t3p_sm[slot], (unsigned long long)(clock64() - (since)))  // per-CTA
 #define T3P_EV(g, ev) do { if (blockIdx.x == 0 && (g) < 64) g_t3trace[(g)][(ev)] = clock64(); } while (0)
+#ifdef GRNND_T3_TRACE_ONLY  // events of CTA 0 only: no per-wait accounting (near-production timing)
+#define T3P_ADD(slot, since)
+#define T3P_WAIT(slot, stmt) stmt
+#else
+#define T3P_ADD(slot, since) atomicAdd(&t3p_sm[slot], (unsigned long long)(clock64() - (since)))  // per-CTA
 #define T3P_WAIT(slot, stmt) do { const long long _w = clock64(); stmt; if (lane == 0) T3P_ADD(slot, _w); } while (0)
+#endif
 #else
 #define T3P_BEGIN()
 #define T3P_ADD(slot, since)
 #define T3P_EV(g, ev)
 #define T3P_WAIT(slot, stmt) stmt
 #endif
-#ifndef GRNND_T3_BULKREC
-#define GRNND_T3_BULKREC 1  // pair records written by bulk stores (TMA); 0: st.global (measured slower)
-#endif
 #ifndef GRNND_T3_NOFILTER
 #define GRNND_T3_NOFILTER 0  // timing experiment only (results invalid): the filter queues nothing
-#endif
-#ifndef GRNND_T3_EARLYREL
-#define GRNND_T3_EARLYREL 0
 #endif
 #ifndef GRNND_T3_PF
 #define GRNND_T3_PF 0
@@ -167,7 +180,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
     if (tid == 0) {
         for (int m = 0; m < NM; ++m) {
             tc::mbar_init(&sm.mfull[m], 1);
-            tc::mbar_init(&sm.mempty[m], 96);
+            tc::mbar_init(&sm.mempty[m], 3 + GRNND_T3_STOREW);  // arrivals: one per warp
         }
         for (int s = 0; s < NS; ++s) {
 #ifdef GRNND_T3_WAITGROUP
@@ -175,13 +188,15 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
 #else
             tc::mbar_init(&sm.full[s], T3_NP * 32);
 #endif
-            tc::mbar_init(&sm.empty[s], 96);
+            tc::mbar_init(&sm.empty[s], 3);
         }
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&sm.accf[b], 1);
-            tc::mbar_init(&sm.acce[b], 96);
-            tc::mbar_init(&sm.qrdy[b], 96);
-            tc::mbar_init(&sm.qemp[b], 96);
+            tc::mbar_init(&sm.recrdy[b], 1);
+            tc::mbar_init(&sm.recfree[b], 1);
+            tc::mbar_init(&sm.acce[b], T3_NF / 32);
+            tc::mbar_init(&sm.qrdy[b], T3_NF / 32);
+            tc::mbar_init(&sm.qemp[b], 3);
         }
         tc::fence_mbar_init();
     }
@@ -234,7 +249,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             }
 #endif
         }
-    } else if (warp >= 11) {
+    } else if (warp >= 11 && warp < 11 + T3_NP) {
         // ================= row producers (9 warps) =================
         // warp pi stages group rows pi, pi + 9, ..: one 512-byte row per instruction (lane =
         // 16-byte chunk, 128-byte swizzle)
@@ -300,9 +315,40 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             }
         }
         __syncwarp();
-    } else if (warp >= 4 && warp <= 6) {
+    } else if (GRNND_T3_STOREW && warp == GRNND_T3_WARPS - 1) {
+        // ================= pair-record bulk stores (for both exact sets) =================
+        if (lane == 0) {
+            const int lcap = list_cap(cap);
+            for (int64_t g = 0; g < nmine; ++g) {
+                const int m = (int)(g % NM), b = (int)(g & 1);
+                const T3Meta &mt = sm.meta[m];
+                tc::mbar_wait(&sm.recrdy[b], (uint32_t)((g >> 1) & 1));
+                tc::fence_proxy_async();  // record writes (generic proxy) -> bulk-store reads
+#pragma unroll
+                for (int pp = 0; pp < GP; ++pp) {
+                    const int64_t v = mt.hdr[pp].x;
+                    if (v < 0) continue;
+                    const int c = sm.rec[b][pp][0];
+                    const int nw = c < lcap ? c : lcap;
+                    const uint32_t bytes = (uint32_t)((16 + 8 * nw + 15) & ~15);
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                                     a.w.clrec + v * (int64_t)CLREC),
+                                 "r"(tc::smem_u32(&sm.rec[b][pp][0])), "r"(bytes)
+                                 : "memory");
+                }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                tc::mbar_arrive(&sm.recfree[b]);
+                tc::mbar_arrive(&sm.mempty[m]);
+            }
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        }
+        __syncwarp();
+    } else if ((warp >= 4 && warp <= 6) || (warp >= 11 + T3_NP && warp < 11 + T3_NP + 3 * GRNND_T3_FSPLIT)) {
         // ================= filter (TMEM lanes 0..95) =================
-        const int fw = warp - 4, i = fw * 32 + lane;
+        // warps 4..6 (and with FSPLIT 20..22: the same TMEM lanes, the other column blocks)
+        const bool fb = warp >= 11 + T3_NP;
+        const int fw = fb ? warp - 11 - T3_NP : warp - 4, i = fw * 32 + lane;
         const float eps_h = a.eps_h + 4.8e-7f;
         for (int64_t g = 0; g < nmine; ++g) {
             const int m = (int)(g % NM), b = (int)(g & 1);
@@ -311,7 +357,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
 #ifdef GRNND_T3_PROF
             const long long _tf0 = clock64();
 #endif
-            {  // this row's filter terms
+            if (!fb) {  // this row's filter terms
                 const int p = i / SZ, sl = i - p * SZ;
                 const bool live = sl < mt.hdr[p].y && mt.ids[i] != TOMB;
                 const float nr = mt.nrm[i];
@@ -326,17 +372,14 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             if (lane == 0) T3P_ADD(22, _tf0);
 #endif
             // queue b free (the exact set of group g - 2 has read it): reset its count
-            T3P_WAIT(6, tc::mbar_wait(&sm.qemp[b], (uint32_t)(((g >> 1) & 1) ^ 1)));
+            if (!fb) T3P_WAIT(6, tc::mbar_wait(&sm.qemp[b], (uint32_t)(((g >> 1) & 1) ^ 1)));
             if (tid == 128) sm.qn[b] = 0;
-            T3P_WAIT(5, tc::named_bar(1, 96));
+            T3P_WAIT(5, tc::named_bar(1, T3_NF));
             T3P_WAIT(7, tc::mbar_wait(&sm.accf[b], (uint32_t)((g >> 1) & 1)));
             if (tid == 128) T3P_EV(g, 4);
             tc::fence_after();
 #ifdef GRNND_T3_PROF
             const long long _tf1 = clock64();
-#endif
-#if GRNND_T3_EARLYREL == 2  // timing experiment only (results invalid): release at MMA completion
-            tc::mbar_arrive(&sm.empty[(int)(g % NS)]);
 #endif
 #ifdef GRNND_T3_PROF
             {  // shared-memory load latency as seen by the filter
@@ -408,16 +451,22 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 // (fw, fw+1); warp 2 takes (0, 2) as its transpose (rows 64.., columns 0..31)
                 const int c0 = fw * 32, c1 = fw < 2 ? fw * 32 + 32 : 0;
                 const bool t1 = fw == 2;
+#if GRNND_T3_FSPLIT
+                const int cb = fb ? c1 : c0;
+                if (cb < kcols) scan32(cb, kcols, fb && t1);
+#else
 #pragma unroll 1
                 for (int h = 0; h < 2; ++h) {  // warp-uniform
                     const int cb = h ? c1 : c0;
                     if (cb < kcols) scan32(cb, kcols, h && t1);
                 }
+#endif
             } else {
                 const int c_lo = ((fw * 32) / SZ) * SZ, c_hi = ((fw * 32 + 31) / SZ + 1) * SZ;
                 const int start = ((c_lo >> 4) << 4) > fw * 32 ? ((c_lo >> 4) << 4) : fw * 32;
+                constexpr int CSTEP = 32 * (1 + GRNND_T3_FSPLIT);
 #pragma unroll 1
-                for (int cb = start; cb < c_hi; cb += 32) scan32(cb, c_hi, false);  // warp-uniform
+                for (int cb = start + (fb ? 32 : 0); cb < c_hi; cb += CSTEP) scan32(cb, c_hi, false);  // warp-uniform
             }
             st_pairs += np;
 #ifdef GRNND_T3_PROF
@@ -425,8 +474,8 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
 #endif
             tc::fence_before();
             if (tid == 128) T3P_EV(g, 5);
-            tc::mbar_arrive(&sm.acce[b]);
-            tc::mbar_arrive(&sm.qrdy[b]);
+            tc::warp_arrive(&sm.acce[b]);
+            tc::warp_arrive(&sm.qrdy[b]);
         }
     } else {
         // ================= exact chains + write-out: two sets of 3 warps =================
@@ -460,10 +509,15 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             const int s = (int)(g % NS), m = (int)(g % NM), b = (int)(g & 1);
             const unsigned char *stg = base + s * T3_STAGE;
             const T3Meta &mt = sm.meta[m];
-            T3P_WAIT(9, tc::mbar_wait(&sm.qrdy[b], (uint32_t)((g >> 1) & 1)));
-#if GRNND_T3_EARLYREL == 1  // timing experiment only (results invalid): release at filter completion
-            tc::mbar_arrive(&sm.empty[s]);
+            if (g >= 2) {  // the previous group's record bulk stores have read the records
+#if GRNND_T3_STOREW
+                tc::mbar_wait(&sm.recfree[b], (uint32_t)(((g >> 1) - 1) & 1));
+#else
+                if (et == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                tc::named_bar(bar_id, 96);
 #endif
+            }
+            T3P_WAIT(9, tc::mbar_wait(&sm.qrdy[b], (uint32_t)((g >> 1) & 1)));
             auto record = [&](int i, int j, float d) {  // pair of group rows i < j, same pool
                 const int p = i / SZ;
                 const int x1 = mt.pos[i], x2 = mt.pos[j];
@@ -490,7 +544,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 const int e = et + NE * t;
                 qk[t] = (qn <= S::QC && e < qn) ? sm.q[b][e] : 0u;
             }
-            tc::mbar_arrive(&sm.qemp[b]);
+            tc::warp_arrive(&sm.qemp[b]);
             if (et == 0) T3P_EV(g, 6);
 #ifdef GRNND_T3_PROF
             const long long _tx0 = clock64();
@@ -584,13 +638,12 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             if (lane == 0) T3P_ADD(18, _tx0);
 #endif
             T3P_WAIT(10, tc::named_bar(bar_id, 96));  // masks + kept distances of group g complete
+            if (et == 0) T3P_EV(g, 8);
 #ifdef GRNND_T3_PROF
             const long long _tx1 = clock64();
 #endif
             // the stage's rows are no longer read: let the producers refill it
-#if !GRNND_T3_EARLYREL
-            tc::mbar_arrive(&sm.empty[s]);
-#endif
+            tc::warp_arrive(&sm.empty[s]);
             // pair records -> global (decide_kernel); masks only for incomplete
             // lists (rare; regular stores); every mask row re-zeroed for the next group
             const int lcap = list_cap(cap);
@@ -611,8 +664,15 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 }
             }
             tc::named_bar(bar_id, 96);  // record headers written
-#if GRNND_T3_BULKREC
+            if (et == 0) T3P_EV(g, 7);
+            // pair records -> global by bulk stores (decide_kernel); their shared-memory reads
+            // are waited for before this set writes records again (next group's start)
+#if GRNND_T3_STOREW
+            if (et == 0) tc::mbar_arrive(&sm.recrdy[b]);
+            if (false) {
+#else
             if (et == 0) {
+#endif
 #pragma unroll
                 for (int pp = 0; pp < GP; ++pp) {
                     const int64_t v = mt.hdr[pp].x;
@@ -626,37 +686,21 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                                  : "memory");
                 }
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // records reusable
             }
-#else
-            // pair records -> global (8-byte stores by the whole set; no async-proxy round trip)
-#pragma unroll
-            for (int pp = 0; pp < GP; ++pp) {
-                const int64_t v = mt.hdr[pp].x;
-                if (v < 0) continue;
-                const int nw = sm.cl_n[b][pp] < lcap ? sm.cl_n[b][pp] : lcap;
-                int2 *dst = reinterpret_cast<int2 *>(a.w.clrec + v * (int64_t)CLREC);
-                const int2 *src = reinterpret_cast<const int2 *>(&sm.rec[b][pp][0]);
-                for (int w = et; w < 2 + nw; w += NE) dst[w] = src[w];
-            }
-#endif
 #ifdef GRNND_T3_PROF
             if (lane == 0) T3P_ADD(19, _tx1);
 #endif
-            tc::named_bar(bar_id, 96);  // masks / counters / metadata read: reset for the next groups
+            if (et == 0) T3P_EV(g, 9);
             if (et == 0) {
 #pragma unroll
                 for (int p = 0; p < GP; ++p) sm.cl_n[b][p] = 0;
             }
-            if (et == 0) T3P_EV(g, 7);
-            tc::mbar_arrive(&sm.mempty[m]);
+            tc::warp_arrive(&sm.mempty[m]);
         }
     }
-#if GRNND_T3_BULKREC
-    if ((warp == 2 || warp == 8) && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-#endif
+    if (!GRNND_T3_STOREW && (warp == 2 || warp == 8) && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 #ifdef GRNND_T3_PROF
-    if (lane == 0) T3P_ADD(warp == 0 ? 1 : warp == 1 ? 17 : (warp >= 4 && warp <= 6) ? 8 : warp >= 11 ? 14 : 11, _t3p0);
+    if (lane == 0) T3P_ADD(warp == 0 ? 1 : warp == 1 ? 17 : (warp >= 4 && warp <= 6) ? 8 : (warp >= 11 && warp < 11 + T3_NP) ? 14 : warp >= 11 ? 25 : 11, _t3p0);
     if (tid == 0) atomicAdd(&t3p_sm[12], (unsigned long long)nmine);
 #endif
     tc::fence_before();

@@ -27,10 +27,10 @@ for r in range(25):
         print(f"round {r + 1}: groups {v[12]}")
         for slot, name, w in rows:
             print(f"   {name:22s} {v[slot] / max(v[12], 1) / w:10.0f} cycles/group")
-tr = (C.c_longlong * 512)()
+tr = (C.c_longlong * 640)()
 lib.grnnd_debug_trace(tr)
-t = np.array(list(tr)).reshape(64, 8)
+t = np.array(list(tr)).reshape(64, 10)
 t0 = t[0, 0]
-print("events (K cycles; CTA 0 of the last bin kernel): 0 meta issued, 1 rows issued (warp 0), 2 rows issued (last warp), 3 mma issued, 4 filter start, 5 filter done, 6 exact start, 7 exact done")
+print("events (K cycles; CTA 0 of the last bin kernel): 0 meta issued, 1 rows issued (warp 0), 2 rows issued (last warp), 3 mma issued, 4 filter start, 5 filter done, 6 exact start, 7 exact done, 8 exact chains done, 9 exact write-out done")
 for gi in range(0, 24):
     print(gi, " ".join(f"{(x - t0) / 1000:8.1f}" for x in t[gi]))
