@@ -56,7 +56,7 @@ constexpr int T3_NP = GRNND_T3_WARPS - 11 - 3 * GRNND_T3_FSPLIT - GRNND_T3_STORE
 constexpr int T3_NF = 96 * (1 + GRNND_T3_FSPLIT);                  // filter threads
 static_assert(!GRNND_T3_FSPLIT || (11 + T3_NP) % 4 == 0, "filter warps must map to TMEM lane quarters 0..2");
 
-struct T3Meta {  // one group's metadata, filled by bulk copies from the staging arrays
+struct alignas(16) T3Meta {  // one group's metadata (staged by tc_stage_kernel, one bulk copy)
     int32_t ids[T3_ROWS];
     float dv[T3_ROWS];
     float nrm[T3_ROWS];
@@ -64,6 +64,7 @@ struct T3Meta {  // one group's metadata, filled by bulk copies from the staging
     int2 hdr[8];  // (vertex row, k) of pool p < GP
 };
 constexpr uint32_t T3_META_BYTES = 3 * 4 * T3_ROWS + T3_ROWS + 64;
+static_assert(sizeof(T3Meta) == T3_META_BYTES && T3_META_BYTES == T3_META_REC, "metadata record layout");
 
 template <int SZ>
 struct T3Smem {
@@ -141,12 +142,6 @@ __device__ long long g_t3trace[64][10];  // CTA 0: per group event times (profil
 #ifndef GRNND_T3_NOFILTER
 #define GRNND_T3_NOFILTER 0  // timing experiment only (results invalid): the filter queues nothing
 #endif
-#ifndef GRNND_T3_PF
-#define GRNND_T3_PF 0
-#endif
-#ifndef GRNND_T3_PF_AHEAD
-#define GRNND_T3_PF_AHEAD 0
-#endif
 
 template <int SZ>
 __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin) {
@@ -223,31 +218,10 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(&sm.mfull[m])),
                              "r"(T3_META_BYTES)
                              : "memory");
-                tc::bulk_g2s(mt.ids, a.w.s_ids + e0, 4 * R, &sm.mfull[m]);
-                tc::bulk_g2s(mt.dv, a.w.s_dv + e0, 4 * R, &sm.mfull[m]);
-                tc::bulk_g2s(mt.nrm, a.w.s_nrm + e0, 4 * R, &sm.mfull[m]);
-                tc::bulk_g2s(mt.pos, a.w.s_pos + e0, R, &sm.mfull[m]);
-                tc::bulk_g2s(mt.hdr, a.w.s_hdr + (e0 / R) * 8, 64, &sm.mfull[m]);
+                tc::bulk_g2s(&mt, a.w.s_meta + (e0 / R) * (int64_t)T3_META_BYTES, T3_META_BYTES, &sm.mfull[m]);
                 T3P_EV(g, 0);
             }
             __syncwarp();
-#if GRNND_T3_PF
-            // L2 prefetch of the group's vector rows, NM - 2 groups ahead of the producers: the
-            // row gathers then land from L2 and a stage is held for less time
-            const int64_t ep = e0 + (int64_t)(GRNND_T3_PF_AHEAD) * G * R;
-            if (ep < (gbase + ngroups) * R) {
-                for (int r = lane; r < R; r += 32) {
-                    const int32_t id = __ldg(a.w.s_ids + ep + r);
-                    if (id == TOMB) continue;
-                    const float *src = a.data + (int64_t)id * a.ld;
-#if GRNND_T3_PF == 1
-                    for (int c = 0; c < nq * 16; c += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"((const char *)src + c));
-#else
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(nq * 16) : "memory");
-#endif
-                }
-            }
-#endif
         }
     } else if (warp >= 11 && warp < 11 + T3_NP) {
         // ================= row producers (9 warps) =================
@@ -679,7 +653,9 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                     if (v < 0) continue;
                     const int nw = sm.cl_n[b][pp] < lcap ? sm.cl_n[b][pp] : lcap;
                     const uint32_t bytes = (uint32_t)((16 + 8 * nw + 15) & ~15);
+#ifndef GRNND_T3_NOFENCE_TEST
                     tc::fence_proxy_async();
+#endif
                     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
                                      a.w.clrec + v * (int64_t)CLREC),
                                  "r"(tc::smem_u32(&sm.rec[b][pp][0])), "r"(bytes)
@@ -749,10 +725,11 @@ __global__ void tc_stage_kernel(PropArgs a) {
             ps = a.w.pos8[(int64_t)vk.x * pcap + s];
             nr = a.norms[id];
         }
-        a.w.s_ids[e] = id;
-        a.w.s_dv[e] = dv;
-        a.w.s_nrm[e] = nr;
-        a.w.s_pos[e] = ps;
-        if (s == 0) a.w.s_hdr[grp * 8 + p] = vk;
+        T3Meta &mt = reinterpret_cast<T3Meta *>(a.w.s_meta)[grp];
+        mt.ids[r] = id;
+        mt.dv[r] = dv;
+        mt.nrm[r] = nr;
+        mt.pos[r] = ps;
+        if (s == 0) mt.hdr[p] = vk;
     }
 }

@@ -15,6 +15,7 @@ constexpr int HEAVY_SEG = 32;  // segments longer than this are sorted by a CTA
 // list_cap(cap)).  A complete list is all decide needs; only when count > list_cap are the
 // full cond / afar masks written as well.  (16-byte aligned records: bulk-stored by tc3.)
 constexpr int PAIR_LIST = 64;
+constexpr int T3_META_REC = 1312;  // sizeof(T3Meta): 96 x (id, dv, norm: 4 B; pos: 1 B) + 8 x int2
 constexpr int CLREC = 4 + 2 * PAIR_LIST;
 __host__ __device__ inline int list_cap(int cap) { return PAIR_LIST < 4 * cap ? PAIR_LIST : 4 * cap; }
 
@@ -55,13 +56,10 @@ struct Workspace {
     uint64_t *cond;      // [n, cap, mw] redirect-condition bits, row = anchor position
     uint64_t *afar;      // [n, cap, mw] "anchor is the farther member" bits
     int32_t *clrec;      // [n, CLREC] redirect-capable pair records (see PAIR_LIST)
-    // tensor-core pair phase (tc3_pairs.cuh): group metadata staged contiguously, 96 slots
-    // per group (only carved when cap <= 96)
-    int32_t *s_ids;
-    float *s_dv;
-    float *s_nrm;
-    uint8_t *s_pos;
-    int2 *s_hdr;         // [groups, 8] (vertex row, k) per pool
+    // tensor-core pair phase (tc3_pairs.cuh): one T3_META_REC-byte metadata record per
+    // group of 96 slots -- pool ids, stored distances, row norms, positions, (vertex, k) per
+    // pool -- fetched by ONE bulk copy (only carved when cap <= 96)
+    unsigned char *s_meta;
     int64_t n;
     int64_t msg_capacity;
 };
@@ -109,11 +107,7 @@ inline size_t carve(Workspace *w, void *base, int64_t n, int32_t cap, int64_t ms
     t.afar = (uint64_t *)take(8 * N * (size_t)(cap > 0 ? cap : 1) * (size_t)t.mw);
     t.clrec = (int32_t *)take(4 * N * (size_t)CLREC);
     const size_t SG = (cap > 0 && cap <= 96) ? N + 8 : 1;  // staging groups (<= one per pool + bins)
-    t.s_ids = (int32_t *)take(4 * SG * 96);
-    t.s_dv = (float *)take(4 * SG * 96);
-    t.s_nrm = (float *)take(4 * SG * 96);
-    t.s_pos = (uint8_t *)take(SG * 96);
-    t.s_hdr = (int2 *)take(8 * 8 * SG);
+    t.s_meta = (unsigned char *)take((size_t)T3_META_REC * SG);
     t.n = n;
     t.msg_capacity = msg_capacity;
     if (w) *w = t;
