@@ -653,9 +653,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                     if (v < 0) continue;
                     const int nw = sm.cl_n[b][pp] < lcap ? sm.cl_n[b][pp] : lcap;
                     const uint32_t bytes = (uint32_t)((16 + 8 * nw + 15) & ~15);
-#ifndef GRNND_T3_NOFENCE_TEST
                     tc::fence_proxy_async();
-#endif
                     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
                                      a.w.clrec + v * (int64_t)CLREC),
                                  "r"(tc::smem_u32(&sm.rec[b][pp][0])), "r"(bytes)
