@@ -194,7 +194,68 @@ __global__ void __launch_bounds__(256) apply_round_kernel(ApplyArgs a) {
             oc.ins += (unsigned long long)base;
             own_total += (unsigned long long)base;
         } else {
-            for (int s0 = 0; s0 < k; s0 += 32) {
+            // Own entries after cnt0 messages from smaller sources.  Until the pool fills, an
+            // own entry is either a duplicate of one of those messages (own entries are
+            // distinct) or appended: a whole chunk is settled with ballots.  From the entry
+            // that would overflow the pool on, the ordered insert() (replacement order).
+            const int cnt0 = P.cnt;
+            int s0 = 0;
+            bool serial = false;
+            for (; s0 < k && !serial; s0 += 32) {
+                const int s = s0 + lane;
+                const int32_t x = s < k ? rid[s] : TOMB;
+                const float xd = s < k ? rd[s] : 0.0f;
+                const int nch = min(32, k - s0);
+                const bool live = x != TOMB;
+                bool dup = false;
+#pragma unroll
+                for (int r = 0; r < RPL; ++r) {
+                    const int lim = min(32, cnt0 - r * 32);  // warp-uniform
+                    for (int jj = 0; jj < lim; ++jj) dup |= __shfl_sync(FULL, P.id[r], jj) == x;
+                }
+                dup = dup && live;
+                const unsigned addm = __ballot_sync(FULL, live && !dup), dupm = __ballot_sync(FULL, dup),
+                               livem = __ballot_sync(FULL, live);
+                const int room = cap - P.cnt;
+                int nbulk = nch;
+                if (__popc(addm) > room) {  // the (room+1)-th append overflows: bulk stops before it
+                    unsigned mm = addm;
+                    for (int t = 0; t < room; ++t) mm &= mm - 1u;
+                    nbulk = __ffs(mm) - 1;
+                    serial = true;
+                }
+                const unsigned pre = nbulk >= 32 ? 0xFFFFFFFFu : ((1u << nbulk) - 1u);
+                const int nadd = __popc(addm & pre);
+                if (lane < nbulk && live && !dup) {
+                    const int p = P.cnt + __popc(addm & ((1u << lane) - 1u));
+                    s_id[wib][p] = x;
+                    s_d[wib][p] = xd;
+                }
+                __syncwarp();
+#pragma unroll
+                for (int r = 0; r < RPL; ++r) {
+                    const int q = r * 32 + lane;
+                    if (q >= P.cnt && q < P.cnt + nadd) {
+                        P.id[r] = s_id[wib][q];
+                        P.d[r] = s_d[wib][q];
+                    }
+                }
+                __syncwarp();
+                if (nadd) P.mxv = false;
+                P.cnt += nadd;
+                oc.ins += (unsigned long long)nadd;
+                oc.dup += (unsigned long long)__popc(dupm & pre);
+                own_total += (unsigned long long)__popc(livem & pre);
+                for (int j = nbulk; j < nch; ++j) {  // only after an overflow
+                    const int32_t cid = __shfl_sync(FULL, x, j);
+                    const float cd = __shfl_sync(FULL, xd, j);
+                    if (cid != TOMB) {
+                        P.insert(cid, cd, oc);
+                        ++own_total;
+                    }
+                }
+            }
+            for (; s0 < k; s0 += 32) {
                 const int s = s0 + lane;
                 const int32_t x = s < k ? rid[s] : TOMB;
                 const float xd = s < k ? rd[s] : 0.0f;
