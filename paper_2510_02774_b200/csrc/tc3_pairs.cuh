@@ -459,14 +459,23 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
         const int et = E ? (warp - 8) * 32 + lane : (warp == 7 ? 64 + lane : (warp - 2) * 32 + lane);  // 0..95
         const int bar_id = 2 + E;
         constexpr int NE = 96;
+        // two chains per thread, the next chunk's four 16-byte loads issued before this chunk's
+        // sums (the shared-memory latency is otherwise exposed once per chunk)
         auto exact2 = [&](const unsigned char *stg, int i1, int j1, int i2, int j2, float &d1, float &d2) {
+            const uint32_t r0 = (uint32_t)((i1 >> 3) * 1024 + (i1 & 7) * 128), q0 = (uint32_t)(i1 & 7);
+            const uint32_t r1 = (uint32_t)((j1 >> 3) * 1024 + (j1 & 7) * 128), q1 = (uint32_t)(j1 & 7);
+            const uint32_t r2 = (uint32_t)((i2 >> 3) * 1024 + (i2 & 7) * 128), q2 = (uint32_t)(i2 & 7);
+            const uint32_t r3 = (uint32_t)((j2 >> 3) * 1024 + (j2 & 7) * 128), q3 = (uint32_t)(j2 & 7);
+            auto ld = [&](uint32_t rb, uint32_t rq, int c) {
+                return *reinterpret_cast<const float4 *>(stg + (uint32_t)(c >> 3) * T3_KB + rb +
+                                                         ((((uint32_t)c & 7u) ^ rq) << 4));
+            };
             float s1 = 0.0f, s2 = 0.0f;
-#pragma unroll 4
+            float4 x1 = ld(r0, q0, 0), y1 = ld(r1, q1, 0), x2 = ld(r2, q2, 0), y2 = ld(r3, q3, 0);
+#pragma unroll 2
             for (int c = 0; c < nq; ++c) {
-                const float4 x1 = *reinterpret_cast<const float4 *>(stg + t3_off(i1, c));
-                const float4 y1 = *reinterpret_cast<const float4 *>(stg + t3_off(j1, c));
-                const float4 x2 = *reinterpret_cast<const float4 *>(stg + t3_off(i2, c));
-                const float4 y2 = *reinterpret_cast<const float4 *>(stg + t3_off(j2, c));
+                const int cn = c + 1 < nq ? c + 1 : c;
+                const float4 nx1 = ld(r0, q0, cn), ny1 = ld(r1, q1, cn), nx2 = ld(r2, q2, cn), ny2 = ld(r3, q3, cn);
                 s1 = exact_step(s1, x1.x, y1.x);
                 s2 = exact_step(s2, x2.x, y2.x);
                 s1 = exact_step(s1, x1.y, y1.y);
@@ -475,6 +484,10 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 s2 = exact_step(s2, x2.z, y2.z);
                 s1 = exact_step(s1, x1.w, y1.w);
                 s2 = exact_step(s2, x2.w, y2.w);
+                x1 = nx1;
+                y1 = ny1;
+                x2 = nx2;
+                y2 = ny2;
             }
             d1 = s1;
             d2 = s2;
