@@ -641,6 +641,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             for (int e = et; e < R * 2; e += NE) {
                 const int r = e >> 1, wd = e & 1;
                 const int pp = r / SZ, x = r - pp * SZ;
+                if (sm.cl_n[b][pp] == 0) continue;  // no record: the pool's mask rows are still zero
                 const int64_t v = mt.hdr[pp].x;
                 const uint64_t cv = sm.cond[b][r][wd], fv = sm.afar[b][r][wd];
                 sm.cond[b][r][wd] = 0ull;
