@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(THREADS) pairs_kernel(PropArgs a, int bin, int
             }
             const int nw = ncl < lcap ? ncl : lcap;
             int32_t *rec = a.w.clrec + v * (int64_t)CLREC;
-            if (tid == 0) rec[0] = ncl;
+            if (tid == 0) a.w.clcnt[v] = ncl;
             for (int e = tid; e < nw; e += THREADS) {
                 rec[4 + 2 * e] = (int32_t)sm.cl_key[g][e];
                 rec[5 + 2 * e] = __float_as_int(sm.cl_d[g][e]);

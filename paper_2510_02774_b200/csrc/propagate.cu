@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) decide_kernel(PropArgs a) {
         // redirect-capable pairs (workspace.cuh PAIR_LIST): a complete list replaces the masks
         const int lcap = list_cap(cap);
         const int32_t *rec = a.w.clrec + v * (int64_t)CLREC;
-        const int ncl_all = rec[0];
+        const int ncl_all = a.w.clcnt[v];
         const bool from_list = ncl_all <= lcap;
         const int ncl = ncl_all < lcap ? ncl_all : lcap;
         int2 e0 = make_int2(0, 0), e1 = make_int2(0, 0);
@@ -626,6 +626,7 @@ int launch_propagate(const PropArgs &a, cudaStream_t st) {
     const int64_t n = a.hi - a.lo;
     if (n <= 0) return GRNND_OK;
     GRNND_CUDA(cudaMemsetAsync(a.w.ctr + C_BIN0, 0, sizeof(unsigned long long) * NBINS, st));
+    GRNND_CUDA(cudaMemsetAsync(a.w.clcnt, 0, sizeof(int32_t) * (size_t)n, st));
     const bool tc3 = GRNND_TC && a.norms && a.dim <= 128 && a.cap <= T3_ROWS && a.order_code == 0;
     const int tb = 128;
     bin_kernel<<<(unsigned)((n + tb - 1) / tb), tb, (size_t)tb * a.cap, st>>>(a.read_count, n, a.cap, a.w, a.stats, a.slice_mode,

@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                     const int64_t v = mt.hdr[pp].x;
                     if (v < 0) continue;
                     const int c = sm.rec[b][pp][0];
+                    if (c == 0) continue;
                     const int nw = c < lcap ? c : lcap;
                     const uint32_t bytes = (uint32_t)((16 + 8 * nw + 15) & ~15);
                     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
@@ -635,8 +636,12 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             // lists (rare; regular stores); every mask row re-zeroed for the next group
             const int lcap = list_cap(cap);
             if (et < GP && mt.hdr[et].x >= 0) {
-                sm.rec[b][et][0] = sm.cl_n[b][et];
-                st_red += (unsigned long long)sm.cl_n[b][et];
+                const int c = sm.cl_n[b][et];
+                sm.rec[b][et][0] = c;
+                if (c > 0) {  // the counts were zeroed for the round
+                    a.w.clcnt[mt.hdr[et].x] = c;
+                    st_red += (unsigned long long)c;
+                }
             }
             for (int e = et; e < R * 2; e += NE) {
                 const int r = e >> 1, wd = e & 1;
@@ -664,7 +669,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
 #pragma unroll
                 for (int pp = 0; pp < GP; ++pp) {
                     const int64_t v = mt.hdr[pp].x;
-                    if (v < 0) continue;
+                    if (v < 0 || sm.cl_n[b][pp] == 0) continue;  // no records: nothing to store
                     const int nw = sm.cl_n[b][pp] < lcap ? sm.cl_n[b][pp] : lcap;
                     const uint32_t bytes = (uint32_t)((16 + 8 * nw + 15) & ~15);
                     tc::fence_proxy_async();

@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_pairs_kernel(PropArgs a, int
             const int nw = ncl < lcap ? ncl : lcap;
             int32_t *rec = a.w.clrec + v * (int64_t)CLREC;
             if (c == 0) {
-                rec[0] = ncl;
+                a.w.clcnt[v] = ncl;
                 red_local += (unsigned long long)ncl;
             }
             if (c < nw) {

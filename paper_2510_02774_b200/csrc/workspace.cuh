@@ -56,6 +56,7 @@ struct Workspace {
     uint64_t *cond;      // [n, cap, mw] redirect-condition bits, row = anchor position
     uint64_t *afar;      // [n, cap, mw] "anchor is the farther member" bits
     int32_t *clrec;      // [n, CLREC] redirect-capable pair records (see PAIR_LIST)
+    int32_t *clcnt;      // [n] their count this round (zeroed per round; the tc3 path writes non-zero only)
     // tensor-core pair phase (tc3_pairs.cuh): one T3_META_REC-byte metadata record per
     // group of 96 slots -- pool ids, stored distances, row norms, positions, (vertex, k) per
     // pool -- fetched by ONE bulk copy (only carved when cap <= 96)
@@ -106,6 +107,7 @@ inline size_t carve(Workspace *w, void *base, int64_t n, int32_t cap, int64_t ms
     t.cond = (uint64_t *)take(8 * N * (size_t)(cap > 0 ? cap : 1) * (size_t)t.mw);
     t.afar = (uint64_t *)take(8 * N * (size_t)(cap > 0 ? cap : 1) * (size_t)t.mw);
     t.clrec = (int32_t *)take(4 * N * (size_t)CLREC);
+    t.clcnt = (int32_t *)take(4 * N);
     const size_t SG = (cap > 0 && cap <= 96) ? N + 8 : 1;  // staging groups (<= one per pool + bins)
     t.s_meta = (unsigned char *)take((size_t)T3_META_REC * SG);
     t.n = n;
