@@ -49,10 +49,7 @@ constexpr int T3_PAD = GRNND_T3_PAD;
 #define GRNND_T3_FSPLIT 0  // 1: warps 20..22 take half of the filter's Gram columns (23 warps)
 #endif
 constexpr int T3_NT = 32 * GRNND_T3_WARPS;
-#ifndef GRNND_T3_STOREW
-#define GRNND_T3_STOREW 0  // 1: the last warp issues the pair-record bulk stores for the exact sets
-#endif
-constexpr int T3_NP = GRNND_T3_WARPS - 11 - 3 * GRNND_T3_FSPLIT - GRNND_T3_STOREW;  // row producers (11..)
+constexpr int T3_NP = GRNND_T3_WARPS - 11 - 3 * GRNND_T3_FSPLIT;  // row producers (11..)
 constexpr int T3_NF = 96 * (1 + GRNND_T3_FSPLIT);                  // filter threads
 static_assert(!GRNND_T3_FSPLIT || (11 + T3_NP) % 4 == 0, "filter warps must map to TMEM lane quarters 0..2");
 
@@ -82,7 +79,6 @@ struct T3Smem {
     uint32_t q[2][QC];            // (row i << 8) | row j
     alignas(16) float psq[6][2][128];  // per exact warp: the squared differences of two pairs
     uint64_t mfull[T3_NM], mempty[T3_NM], full[T3_NS], empty[T3_NS], accf[2], acce[2], qrdy[2], qemp[2];
-    uint64_t recrdy[2], recfree[2];  // records of a group complete / read by the bulk stores (STOREW)
     uint32_t tmem_base;
 };
 
@@ -175,7 +171,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
     if (tid == 0) {
         for (int m = 0; m < NM; ++m) {
             tc::mbar_init(&sm.mfull[m], 1);
-            tc::mbar_init(&sm.mempty[m], 3 + GRNND_T3_STOREW);  // arrivals: one per warp
+            tc::mbar_init(&sm.mempty[m], 3);  // arrivals: one per warp
         }
         for (int s = 0; s < NS; ++s) {
 #ifdef GRNND_T3_WAITGROUP
@@ -187,8 +183,6 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
         }
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&sm.accf[b], 1);
-            tc::mbar_init(&sm.recrdy[b], 1);
-            tc::mbar_init(&sm.recfree[b], 1);
             tc::mbar_init(&sm.acce[b], T3_NF / 32);
             tc::mbar_init(&sm.qrdy[b], T3_NF / 32);
             tc::mbar_init(&sm.qemp[b], 3);
@@ -287,36 +281,6 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 T3P_EV(g, 3);
                 T3P_WAIT(21, tc::mma_commit(&sm.accf[ac]));
             }
-        }
-        __syncwarp();
-    } else if (GRNND_T3_STOREW && warp == GRNND_T3_WARPS - 1) {
-        // ================= pair-record bulk stores (for both exact sets) =================
-        if (lane == 0) {
-            const int lcap = list_cap(cap);
-            for (int64_t g = 0; g < nmine; ++g) {
-                const int m = (int)(g % NM), b = (int)(g & 1);
-                const T3Meta &mt = sm.meta[m];
-                tc::mbar_wait(&sm.recrdy[b], (uint32_t)((g >> 1) & 1));
-                tc::fence_proxy_async();  // record writes (generic proxy) -> bulk-store reads
-#pragma unroll
-                for (int pp = 0; pp < GP; ++pp) {
-                    const int64_t v = mt.hdr[pp].x;
-                    if (v < 0) continue;
-                    const int c = sm.rec[b][pp][0];
-                    if (c == 0) continue;
-                    const int nw = c < lcap ? c : lcap;
-                    const uint32_t bytes = (uint32_t)((16 + 8 * nw + 15) & ~15);
-                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
-                                     a.w.clrec + v * (int64_t)CLREC),
-                                 "r"(tc::smem_u32(&sm.rec[b][pp][0])), "r"(bytes)
-                                 : "memory");
-                }
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                tc::mbar_arrive(&sm.recfree[b]);
-                tc::mbar_arrive(&sm.mempty[m]);
-            }
-            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         }
         __syncwarp();
     } else if ((warp >= 4 && warp <= 6) || (warp >= 11 + T3_NP && warp < 11 + T3_NP + 3 * GRNND_T3_FSPLIT)) {
@@ -497,13 +461,13 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             const int s = (int)(g % NS), m = (int)(g % NM), b = (int)(g & 1);
             const unsigned char *stg = base + s * T3_STAGE;
             const T3Meta &mt = sm.meta[m];
-            if (g >= 2) {  // the previous group's record bulk stores have read the records
-#if GRNND_T3_STOREW
-                tc::mbar_wait(&sm.recfree[b], (uint32_t)(((g >> 1) - 1) & 1));
-#else
-                if (et == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            if (g >= 2) {  // group g - 2: record bulk stores have read the records, masks cleared
+                if (et == 0) {
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#pragma unroll
+                    for (int p = 0; p < GP; ++p) sm.cl_n[b][p] = 0;
+                }
                 tc::named_bar(bar_id, 96);
-#endif
             }
             T3P_WAIT(9, tc::mbar_wait(&sm.qrdy[b], (uint32_t)((g >> 1) & 1)));
             auto record = [&](int i, int j, float d) {  // pair of group rows i < j, same pool
@@ -656,16 +620,11 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                     a.w.afar[(v * cap + x) * mw + wd] = fv;
                 }
             }
-            tc::named_bar(bar_id, 96);  // record headers written
+            if (et < 32) __syncwarp();  // record headers (written by this warp) -> bulk stores
             if (et == 0) T3P_EV(g, 7);
             // pair records -> global by bulk stores (decide_kernel); their shared-memory reads
             // are waited for before this set writes records again (next group's start)
-#if GRNND_T3_STOREW
-            if (et == 0) tc::mbar_arrive(&sm.recrdy[b]);
-            if (false) {
-#else
             if (et == 0) {
-#endif
 #pragma unroll
                 for (int pp = 0; pp < GP; ++pp) {
                     const int64_t v = mt.hdr[pp].x;
@@ -684,14 +643,10 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             if (lane == 0) T3P_ADD(19, _tx1);
 #endif
             if (et == 0) T3P_EV(g, 9);
-            if (et == 0) {
-#pragma unroll
-                for (int p = 0; p < GP; ++p) sm.cl_n[b][p] = 0;
-            }
             tc::warp_arrive(&sm.mempty[m]);
         }
     }
-    if (!GRNND_T3_STOREW && (warp == 2 || warp == 8) && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if ((warp == 2 || warp == 8) && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 #ifdef GRNND_T3_PROF
     if (lane == 0) T3P_ADD(warp == 0 ? 1 : warp == 1 ? 17 : (warp >= 4 && warp <= 6) ? 8 : (warp >= 11 && warp < 11 + T3_NP) ? 14 : warp >= 11 ? 25 : 11, _t3p0);
     if (tid == 0) atomicAdd(&t3p_sm[12], (unsigned long long)nmine);
