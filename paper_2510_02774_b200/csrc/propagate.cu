@@ -29,8 +29,8 @@
 namespace grnnd {
 
 __device__ __forceinline__ int bin_of(int k, int tc_bins) {
-    if (tc_bins)  // tensor-core groups of 96 rows: slot sizes 16, 24, 32, 48, 96 (tc3_pairs.cuh)
-        return k <= 1 ? 0 : k <= 16 ? 1 : k <= 24 ? 2 : k <= 32 ? 3 : k <= 48 ? 4 : 5;
+    if (tc_bins)  // tensor-core groups of 96 rows: slot sizes 8, 16, 24, 32, 48, 96 (tc3_pairs.cuh)
+        return k <= 1 ? 0 : k <= 8 ? 1 : k <= 16 ? 2 : k <= 24 ? 3 : k <= 32 ? 4 : k <= 48 ? 5 : 6;
     return k <= 1 ? 0 : k <= 16 ? 1 : k <= 32 ? 2 : k <= 64 ? 3 : k <= 128 ? 4 : 5;
 }
 
@@ -639,11 +639,12 @@ int launch_propagate(const PropArgs &a, cudaStream_t st) {
     if (tc3) {
         tc_stage_kernel<<<sm_count() * 8, 256, 0, st>>>(a);
         GRNND_TRY(check_launch("tc_stage_kernel"));
-        if (a.cap > 48) GRNND_TRY(launch_tc3_pairs<96>(a, 5, st));
-        if (a.cap > 32) GRNND_TRY(launch_tc3_pairs<48>(a, 4, st));
-        if (a.cap > 24) GRNND_TRY(launch_tc3_pairs<32>(a, 3, st));
-        if (a.cap > 16) GRNND_TRY(launch_tc3_pairs<24>(a, 2, st));
-        if (a.cap > 1) GRNND_TRY(launch_tc3_pairs<16>(a, 1, st));
+        if (a.cap > 48) GRNND_TRY(launch_tc3_pairs<96>(a, 6, st));
+        if (a.cap > 32) GRNND_TRY(launch_tc3_pairs<48>(a, 5, st));
+        if (a.cap > 24) GRNND_TRY(launch_tc3_pairs<32>(a, 4, st));
+        if (a.cap > 16) GRNND_TRY(launch_tc3_pairs<24>(a, 3, st));
+        if (a.cap > 8) GRNND_TRY(launch_tc3_pairs<16>(a, 2, st));
+        if (a.cap > 1) GRNND_TRY(launch_tc3_pairs<8>(a, 1, st));
     } else if (GRNND_TC && a.norms && a.dim <= 128 && a.cap <= 128 && a.order_code == 0) {
         if (a.cap > 64) GRNND_TRY(launch_tc_pairs<128>(a, 4, st));
         if (a.cap > 32) GRNND_TRY(launch_tc_pairs<64>(a, 3, st));

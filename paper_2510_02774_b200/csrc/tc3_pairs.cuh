@@ -21,7 +21,7 @@
 //   warps 4-6    filter (TMEM lanes 0..95): Gram -> band candidates -> queue g % 2;
 //   warps 2,3,7 / 8,9,10  two exact sets (even / odd groups): exact chains of the queue ->
 //                redirect records -> global (bulk stores); release the stage and meta slot.
-// Groups: 96 rows = one pool of k <= 96, or 96/SZ pools of k <= SZ (SZ = 16, 24, 32, 48).
+// Groups: 96 rows = one pool of k <= 96, or 96/SZ pools of k <= SZ (SZ = 8, 16, 24, 32, 48).
 #pragma once
 
 constexpr int T3_ROWS = 96;
@@ -58,22 +58,25 @@ struct alignas(16) T3Meta {  // one group's metadata (staged by tc_stage_kernel,
     float dv[T3_ROWS];
     float nrm[T3_ROWS];
     uint8_t pos[T3_ROWS];
-    int2 hdr[8];  // (vertex row, k) of pool p < GP
+    int2 hdr[12];  // (vertex row, k) of pool p < GP
 };
-constexpr uint32_t T3_META_BYTES = 3 * 4 * T3_ROWS + T3_ROWS + 64;
+constexpr uint32_t T3_META_BYTES = 3 * 4 * T3_ROWS + T3_ROWS + 96;
 static_assert(sizeof(T3Meta) == T3_META_BYTES && T3_META_BYTES == T3_META_REC, "metadata record layout");
 
 template <int SZ>
 struct T3Smem {
     static constexpr int GP = T3_ROWS / SZ;
-    static constexpr int CL = PAIR_LIST;  // redirect-capable pairs handed to decide (workspace.cuh)
+    // redirect-capable pairs handed to decide (workspace.cuh); a pool of k <= SZ has at most
+    // SZ (SZ - 1) / 2 pairs, so small slots never truncate a list
+    static constexpr int CL = PAIR_LIST < SZ * (SZ - 1) / 2 ? PAIR_LIST : SZ * (SZ - 1) / 2;
+    static constexpr int RS = 4 + 2 * CL;  // record stride (int32), a multiple of 4
     static constexpr int QC = 512;   // filter candidates per group (overflow: exact sweep)
     T3Meta meta[T3_NM];
     float2 ab[2][T3_ROWS];        // filter terms (A = -inf: always a candidate; B = -1: dead row)
     uint32_t livec[2][4];         // bit r: row r's B >= 0 (a column that can pair)
     uint64_t cond[2][T3_ROWS][2];  // per exact set: row = p * SZ + anchor position; bit = partner
     uint64_t afar[2][T3_ROWS][2];
-    alignas(16) int32_t rec[2][GP][CLREC];  // per exact set, per pool: pair records (workspace.cuh)
+    alignas(16) int32_t rec[2][GP][RS];  // per exact set, per pool: pair records (workspace.cuh layout)
     int cl_n[2][GP];
     int qn[2];
     uint32_t q[2][QC];            // (row i << 8) | row j
@@ -104,10 +107,11 @@ __device__ __forceinline__ uint32_t t3_off(int r, int c) {
     return (uint32_t)((c >> 3) * T3_KB + (r >> 3) * 1024 + (r & 7) * 128 + (((c & 7) ^ (r & 7)) << 4));
 }
 
-// TC bins 1..5 (slot sizes 16, 24, 32, 48, 96): groups of bin b start at staging group
+// TC bins 1..6 (slot sizes 8, 16, 24, 32, 48, 96): groups of bin b start at staging group
 // tc_group_base(b) (all bins' groups back to back)
-__host__ __device__ __forceinline__ int tc_bin_gp(int b) { return b == 1 ? 6 : b == 2 ? 4 : b == 3 ? 3 : b == 4 ? 2 : 1; }
+__host__ __device__ __forceinline__ int tc_bin_gp(int b) { return b == 1 ? 12 : b == 2 ? 6 : b == 3 ? 4 : b == 4 ? 3 : b == 5 ? 2 : 1; }
 __host__ __device__ __forceinline__ int tc_bin_sz(int b) { return 96 / tc_bin_gp(b); }
+constexpr int T3_NBINS = 6;  // TC bins 1..6: slot sizes 8, 16, 24, 32, 48, 96
 __device__ __forceinline__ int64_t tc_group_base(const unsigned long long *ctr, int b) {
     int64_t base = 0;
     for (int x = 1; x < b; ++x) {
@@ -672,16 +676,16 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
 // of its pools.  Thread per staging slot: reads of a pool's row are coalesced.
 __global__ void tc_stage_kernel(PropArgs a) {
     const unsigned long long *ctr = a.w.ctr;
-    int64_t gb[7];
+    int64_t gb[T3_NBINS + 2];
     gb[1] = 0;
-    for (int b = 1; b <= 5; ++b) gb[b + 1] = gb[b] + ((int64_t)ctr[C_BIN0 + b] + tc_bin_gp(b) - 1) / tc_bin_gp(b);
-    const int64_t total = gb[6] * T3_ROWS;
+    for (int b = 1; b <= T3_NBINS; ++b) gb[b + 1] = gb[b] + ((int64_t)ctr[C_BIN0 + b] + tc_bin_gp(b) - 1) / tc_bin_gp(b);
+    const int64_t total = gb[T3_NBINS + 1] * T3_ROWS;
     const int cap = a.cap, pcap = a.w.pcap;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t grp = e / T3_ROWS;
         const int r = (int)(e - grp * T3_ROWS);
         int b = 1;
-        while (b < 5 && grp >= gb[b + 1]) ++b;
+        while (b < T3_NBINS && grp >= gb[b + 1]) ++b;
         const int sz = tc_bin_sz(b), gp = tc_bin_gp(b);
         const int p = r / sz, s = r - p * sz;
         const int64_t posn = (grp - gb[b]) * gp + p;  // position in bin b's list

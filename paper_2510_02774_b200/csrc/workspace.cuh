@@ -15,7 +15,7 @@ constexpr int HEAVY_SEG = 32;  // segments longer than this are sorted by a CTA
 // list_cap(cap)).  A complete list is all decide needs; only when count > list_cap are the
 // full cond / afar masks written as well.  (16-byte aligned records: bulk-stored by tc3.)
 constexpr int PAIR_LIST = 64;
-constexpr int T3_META_REC = 1312;  // sizeof(T3Meta): 96 x (id, dv, norm: 4 B; pos: 1 B) + 8 x int2
+constexpr int T3_META_REC = 1344;  // sizeof(T3Meta): 96 x (id, dv, norm: 4 B; pos: 1 B) + 12 x int2
 constexpr int CLREC = 4 + 2 * PAIR_LIST;
 __host__ __device__ inline int list_cap(int cap) { return PAIR_LIST < 4 * cap ? PAIR_LIST : 4 * cap; }
 
