@@ -40,7 +40,7 @@ METRIC = "build seconds at 1M×128 (1/2/4/8 B200); graph recall@10 vs CPU ref"
 WORKLOAD = "SIFT1M-shape synthetic 1M×128 fp32 L2, R=96, single B200"
 PARAMS = dict(S=20, R=96, T1=4, T2=15, rho=0.6, seed=1)
 PAIRS_FILE = ROOT / "profiles" / "c2_round_pairs.json"
-NCU_FILE = ROOT / "profiles" / "r1e_pair_phase_ncu.json"
+NCU_FILE = ROOT / "profiles" / "r1f_pair_phase_ncu.json"
 CPU_PROFILE = ROOT / "profiles" / "c2_cpu_rounds.json"
 
 

@@ -13,9 +13,9 @@ timeout 600 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/$
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
    python bench.py --no-cpu --steps 1 --warmup 1 > gpurun_out/${TAG}_bench_under_ncu.log 2>&1
 python tools/launch_summary.py gpurun_out/${TAG}_launches.csv > gpurun_out/${TAG}_launch_summary.txt 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tc3_pairs|tc_stage|decide" -s 122 -c 7 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tc3_pairs|tc_stage|decide" -s 139 -c 8 \
    -o gpurun_out/${TAG}_round_full -f python tools/prof_rounds.py 1000000 128 2 15 > gpurun_out/${TAG}_ncu_full.log 2>&1
 python tools/ncu_to_json.py gpurun_out/${TAG}_round_full.ncu-rep gpurun_out/${TAG}_pair_phase_ncu.json \
-   "ncu --set full --clock-control none -k regex:tc3_pairs|tc_stage|decide -s 122 -c 7, tools/prof_rounds.py 1000000 128 2 15 (update round 21)" \
+   "ncu --set full --clock-control none -k regex:tc3_pairs|tc_stage|decide -s 139 -c 8, tools/prof_rounds.py 1000000 128 2 15 (update round 21)" \
    > gpurun_out/${TAG}_ncu_json.log 2>&1
 echo done
