@@ -35,7 +35,7 @@ constexpr int T3_NS = 4;              // row stages
 #define GRNND_T3_PAD 0
 #endif
 #ifndef GRNND_T3_WCOOP
-#define GRNND_T3_WCOOP 24
+#define GRNND_T3_WCOOP 16
 #endif
 constexpr int T3_WCOOP = GRNND_T3_WCOOP;  // queues up to this length: warp-cooperative chains (<= 32)
 constexpr int T3_NM = GRNND_T3_NM;    // metadata slots
