@@ -60,6 +60,9 @@ enum {
     GRNND_ST_CANDIDATES = 10, /* pairs the filtered pair phase re-evaluated exactly (instrumentation) */
     GRNND_ST_OVERFLOWS = 11,  /* groups whose candidate queue overflowed into an exact sweep */
     GRNND_ST_REDIRECTABLE = 12, /* pairs meeting the redirect condition (instrumentation)      */
+    GRNND_ST_LOST = 13,       /* messages a round could not hold (emit list beyond msg_capacity)
+                                 or that reached the wrong rank: non-zero = the round is invalid,
+                                 the Python layer raises DeviceError (GRNND_EWORKSPACE meaning) */
     GRNND_NSTATS = 16
 };
 
@@ -197,11 +200,13 @@ int grnnd_round_emit(const grnnd_pools *p, int32_t kind /*0 update, 1 reverse*/,
                      uint64_t stream_id, int32_t order_code, double rho,
                      const int64_t *rank_bounds /*device int64[nranks+1]*/, int32_t nranks,
                      int64_t *send_counts /*device int64[nranks]*/, grnnd_stream_t s);
-/* device pointers to the outgoing (bucketed by rank) and incoming message arrays inside
- * the workspace: key int64, tgt int32, id int32, dist fp32 */
-int grnnd_round_buffers(const grnnd_pools *p, int64_t **out_key, int32_t **out_tgt,
-                        int32_t **out_id, float **out_dist, int64_t **in_key, int32_t **in_tgt,
-                        int32_t **in_id, float **in_dist);
+/* Device pointers to the packed outgoing (bucketed by rank, send_counts[r] messages for
+ * rank r in rank order) and incoming message buffers inside the workspace; each message is
+ * GRNND_MSG_WORDS int32 (key low, key high, tgt, id, dist bits), so one all-to-all moves a
+ * round's payload.  Capacity: msg_capacity messages each. */
+#define GRNND_MSG_WORDS 5
+int grnnd_round_buffers(const grnnd_pools *p, int32_t **out_pack, int32_t **in_pack);
+/* Apply the n_incoming packed messages received (in source-rank order) in in_pack. */
 int grnnd_round_apply(const grnnd_pools *p, int32_t kind, int64_t n_incoming, grnnd_stream_t s);
 
 /* builder.finalize_graph (:342-362): rows sorted by (dist, id) into CSR.
@@ -225,6 +230,37 @@ int grnnd_check_finite(const float *data, int64_t n, int32_t dim, int32_t ld, in
 /* Row-sorted fixed-degree view (the fixed-degree int32 [n, cap] adjacency, -1 padded). */
 int grnnd_sorted_rows(const int32_t *ids, const float *dists, const int32_t *counts, int64_t n,
                       int32_t cap, int32_t *out_ids, grnnd_stream_t s);
+
+/* ------------------------------------------------------------------------ */
+/* (3) evaluation kernels (csrc/search.cu)                                   */
+/* ------------------------------------------------------------------------ */
+
+/* _numba_kernels.brute_force (:384-413) / search.brute_force_knn_batch (search.py:130-142):
+ * exact k nearest ids of queries[nq, ld] among data[n, ld] (first dim columns, zero padded),
+ * ties broken by ascending id; out_ids int32[nq, k], out_dists fp32[nq, k] (nullable).
+ * 1 <= k <= min(n, 64). */
+size_t grnnd_brute_force_workspace_bytes(int64_t n, int64_t nq, int32_t k);
+int grnnd_brute_force(const float *data, int64_t n, int32_t dim, int32_t ld, const float *queries, int64_t nq,
+                      int32_t k, int32_t *out_ids, float *out_dists, void *workspace, size_t workspace_bytes,
+                      grnnd_stream_t s);
+
+/* _numba_kernels.greedy_search_batch / _greedy_single (:416-513), search.search_batch
+ * (search.py:90-115): best-first search with a candidate list of L keys ordered by
+ * (dist, id) from entries[q] over the CSR graph (offsets int64[n+1], nbrs int32).
+ * out_ids int32[nq, k] / out_dists fp32[nq, k] (nullable) are written for the first
+ * out_cnt[q] = min(k, list size) ranks, -1 / inf after.  visited: >= grnnd_search_visited_bytes
+ * (zeroed by the call).  L <= 1024. */
+size_t grnnd_search_visited_bytes(int64_t n, int64_t nq);
+int grnnd_greedy_search(const int64_t *offsets, const int32_t *nbrs, int64_t n, const float *data, int32_t dim,
+                        int32_t ld, const float *queries, int64_t nq, int32_t L, int32_t k, const int64_t *entries,
+                        int32_t *out_ids, float *out_dists, int64_t *out_cnt, void *visited, size_t visited_bytes,
+                        grnnd_stream_t s);
+
+/* Inner-product metric (not in the reference, SURVEY 7 hard part 6): scale each row of
+ * data[n, ld] in place to unit L2 norm (sequential fp32 sum of squares, correctly rounded
+ * sqrt and division; zero rows unchanged), so squared L2 = 2 - 2<a, b> and the L2 build is
+ * the IP build. */
+int grnnd_normalize_rows(float *data, int64_t n, int32_t dim, int32_t ld, grnnd_stream_t s);
 
 #ifdef __cplusplus
 }

@@ -95,6 +95,7 @@ def lib():
             _i32,
             [_f32p, _i64, _i32, _i32, _i32, _i32, _i32, C.c_double, _u64, _i32, _i64p, _i32p, C.c_void_p],
         ),
+        "orc_normalize_rows": (None, [_f32p, _i64, _i32]),
         "orc_brute_force": (None, [_f32p, _i64, _i32, _f32p, _i64, _i32, _i32p]),
         "orc_greedy_search": (
             None, [_i64p, _i32p, _f32p, _i64, _i32, _f32p, _i64, _i32, _i32, _i64p, _i32p]
@@ -348,6 +349,13 @@ class State:
         if p:
             lib().orc_state_free(p)
             self._p = None
+
+
+def normalize_rows(data) -> np.ndarray:
+    """IP metric: a copy of ``data`` with unit-norm rows (orc_normalize_rows)."""
+    x = np.array(data, dtype=np.float32, order="C", copy=True)
+    lib().orc_normalize_rows(x, x.shape[0], x.shape[1])
+    return x
 
 
 def brute_force_knn(data, queries, k):

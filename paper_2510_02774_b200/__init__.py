@@ -44,7 +44,15 @@ from .builder import (  # noqa: E402  (loads libgrnnd_b200.so; raises if it is n
     update_round,
     validate_state,
 )
-
+from .search import (  # noqa: E402
+    SearchParams,
+    brute_force_knn,
+    brute_force_knn_batch,
+    greedy_search,
+    mean_recall,
+    recall_at_k,
+    search_batch,
+)
 
 __all__ = [
     "BuildParams", "BuildState", "Dataset", "DeviceError", "DimensionMismatch", "DoubleBufferPool",
@@ -52,4 +60,6 @@ __all__ = [
     "RoundStats", "SelfInsert", "TOMBSTONE", "build", "build_fixed_degree", "cooperative_insert",
     "effective_params", "finalize_graph", "generate", "init_neighbors", "reverse_edge_sampling",
     "rng_redirect_check", "update_round", "validate_params", "validate_state",
+    "SearchParams", "brute_force_knn", "brute_force_knn_batch", "greedy_search", "mean_recall", "recall_at_k",
+    "search_batch",
 ]

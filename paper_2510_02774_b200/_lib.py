@@ -22,6 +22,8 @@ NSTATS = 16
 ST_MESSAGES, ST_REDIRECTS, ST_SURVIVORS, ST_REVERSE_ATTEMPTS = 0, 1, 2, 3
 ST_INSERTED, ST_DUPLICATE, ST_REPLACED, ST_REJECTED = 4, 5, 6, 7
 ST_PAIRS, ST_PAIRS_REF, ST_CANDIDATES, ST_OVERFLOWS = 8, 9, 10, 11
+ST_REDIRECTABLE, ST_LOST = 12, 13
+MSG_WORDS = 5
 MAX_CAP = 256
 
 _vp = C.c_void_p
@@ -83,16 +85,20 @@ _SIGS = {
     "grnnd_update_round": (C.c_int, [C.POINTER(Pools), _u64, _u64, _i32, _vp]),
     "grnnd_reverse_round": (C.c_int, [C.POINTER(Pools), _dbl, _vp]),
     "grnnd_round_emit": (C.c_int, [C.POINTER(Pools), _i32, _u64, _u64, _i32, _dbl, _vp, _i32, _vp, _vp]),
-    "grnnd_round_buffers": (
-        C.c_int,
-        [C.POINTER(Pools)] + [C.POINTER(_vp)] * 8,
-    ),
+    "grnnd_round_buffers": (C.c_int, [C.POINTER(Pools), C.POINTER(_vp), C.POINTER(_vp)]),
     "grnnd_round_apply": (C.c_int, [C.POINTER(Pools), _i32, _i64, _vp]),
     "grnnd_finalize": (C.c_int, [_vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "grnnd_sorted_rows": (C.c_int, [_vp, _vp, _vp, _i64, _i32, _vp, _vp]),
     "grnnd_finalize_pools": (C.c_int, [C.POINTER(Pools), _vp, _vp, _vp, _vp]),
     "grnnd_check_finite": (C.c_int, [_vp, _i64, _i32, _i32, _vp, _vp]),
     "grnnd_row_norms": (C.c_int, [_vp, _i64, _i32, _i32, _vp, _vp]),
+    "grnnd_brute_force_workspace_bytes": (_sz, [_i64, _i64, _i32]),
+    "grnnd_brute_force": (C.c_int, [_vp, _i64, _i32, _i32, _vp, _i64, _i32, _vp, _vp, _vp, _sz, _vp]),
+    "grnnd_search_visited_bytes": (_sz, [_i64, _i64]),
+    "grnnd_greedy_search": (
+        C.c_int, [_vp, _vp, _i64, _vp, _i32, _i32, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+    ),
+    "grnnd_normalize_rows": (C.c_int, [_vp, _i64, _i32, _i32, _vp]),
 }
 
 if not LIB_PATH.exists():

@@ -92,6 +92,9 @@ class RoundStats:
     @classmethod
     def from_counters(cls, kind: str, c) -> "RoundStats":
         c = [int(x) for x in c]
+        if c[_lib.ST_LOST]:
+            raise DeviceError(f"{kind} round lost {c[_lib.ST_LOST]} message(s): the message capacity of the "
+                              "workspace is too small for this round (GRNND_EWORKSPACE)")
         st = cls(
             kind=kind,
             messages=c[_lib.ST_MESSAGES],
@@ -179,6 +182,34 @@ def check_finite_device(data_dev: torch.Tensor, dim: int) -> None:
 
 
 EXACT_FIRST_ROUNDS = 3  # update rounds (stream ids 1..3) that run the exact-only pair phase
+METRICS = ("l2", "ip")
+
+
+def check_metric(metric: str) -> None:
+    if metric not in METRICS:
+        raise ParamError(f"metric must be one of {METRICS}, got {metric!r}")
+
+
+def normalize_rows_(data_dev: torch.Tensor, dim: int) -> torch.Tensor:
+    """IP metric (SURVEY 7 hard part 6; the reference has L2 only): rows scaled in place to
+    unit norm on the device, so the squared L2 the build uses is 2 - 2<a, b>."""
+    n, ld = data_dev.shape
+    with torch.cuda.device(data_dev.device):
+        _lib.call("grnnd_normalize_rows", data_dev.data_ptr(), n, dim, ld, _stream(data_dev.device))
+    return data_dev
+
+
+def _on_device(method):
+    """Run a pools method with the pools' device current: the library launches onto that
+    device's current stream, and the CUDA runtime's current device must match it."""
+    import functools
+
+    @functools.wraps(method)
+    def wrapper(self, *a, **k):
+        with torch.cuda.device(self.dev):
+            return method(self, *a, **k)
+
+    return wrapper
 
 
 class _DevicePools:
@@ -217,8 +248,14 @@ class _DevicePools:
         self.norms = None
         if filtered:
             self.norms = torch.empty(self.n_total, dtype=f32, device=dev)
-            _lib.call("grnnd_row_norms", data_dev.data_ptr(), self.n_total, self.dim, self.ld,
-                      self.norms.data_ptr(), _stream(dev))
+            self.compute_norms()
+
+    def compute_norms(self) -> None:
+        """Squared row norms of the vectors (the tensor-core pre-screen's |a|^2 terms)."""
+        if self.norms is not None:
+            with torch.cuda.device(self.dev):
+                _lib.call("grnnd_row_norms", self.data.data_ptr(), self.n_total, self.dim, self.ld,
+                          self.norms.data_ptr(), _stream(self.dev))
 
     def struct(self, stats: torch.Tensor | None = None, filtered: bool = True) -> _lib.Pools:
         norms = self.norms if filtered else None
@@ -249,23 +286,27 @@ class _DevicePools:
         self.write_count.zero_()
 
     # -- the four asynchronous steps --
+    @_on_device
     def init(self, S: int, seed: int) -> torch.Tensor:
         fail = torch.zeros(1, dtype=torch.int64, device=self.dev)
         p = self.struct()
         _lib.call("grnnd_init_pools", C.byref(p), S, seed & MASK64, fail.data_ptr(), _stream(self.dev))
         return fail
 
+    @_on_device
     def update(self, seed: int, stream_id: int, order_code: int, stats: torch.Tensor) -> None:
         p = self.struct(stats, self.filtered_round(stream_id))
         _lib.call("grnnd_update_round", C.byref(p), seed & MASK64, stream_id & MASK64, order_code,
                   _stream(self.dev))
         self.swap()
 
+    @_on_device
     def reverse(self, rho: float, stats: torch.Tensor) -> None:
         p = self.struct(stats)
         _lib.call("grnnd_reverse_round", C.byref(p), float(rho), _stream(self.dev))
         self.swap()
 
+    @_on_device
     def update_split(self, seed: int, stream_id: int, order_code: int, stats: torch.Tensor,
                      ev: tuple | None = None) -> None:
         """update() as its two halves with optional CUDA events (before emit, after emit,
@@ -282,11 +323,13 @@ class _DevicePools:
             ev[2].record()
         self.swap()
 
+    @_on_device
     def finalize(self, offsets: torch.Tensor, nbrs: torch.Tensor, bad: torch.Tensor) -> None:
         p = self.struct()
         _lib.call("grnnd_finalize_pools", C.byref(p), offsets.data_ptr(), nbrs.data_ptr(), bad.data_ptr(),
                   _stream(self.dev))
 
+    @_on_device
     def sorted_rows(self) -> torch.Tensor:
         out = torch.empty((self.rows, self.cap), dtype=torch.int32, device=self.dev)
         _lib.call("grnnd_sorted_rows", self.read_ids.data_ptr(), self.read_dists.data_ptr(),
@@ -392,18 +435,24 @@ class BuildState:
 
 
 def init_neighbors(dataset: Dataset, params: BuildParams, pair_order: PairOrder = "disordered",
-                   *, device=None) -> BuildState:
-    """S distinct random neighbours != owner per vertex (builder.py:221-257)."""
+                   *, device=None, metric: str = "l2") -> BuildState:
+    """S distinct random neighbours != owner per vertex (builder.py:221-257).  The
+    reference validates the dataset (finiteness included) before the parameters; so does
+    this, with the finiteness scan on the device."""
     dataset.validate_shape()
     n = dataset.num_points
-    validate_params(params, n)
-    if params.S > n - 1:
-        raise ParamError("S <= N-1")
     if pair_order not in _ORDER_CODES:
         raise ParamError(f"pair_order must be one of {sorted(_ORDER_CODES)}")
+    check_metric(metric)
     dev = _device(device)
-    data_dev = upload(dataset.data, dev)
-    check_finite_device(data_dev, dataset.dim)
+    with torch.cuda.device(dev):
+        data_dev = upload(dataset.data, dev)
+        check_finite_device(data_dev, dataset.dim)
+        validate_params(params, n)
+        if params.S > n - 1:
+            raise ParamError("S <= N-1")
+        if metric == "ip":
+            normalize_rows_(data_dev, dataset.dim)
     pools = _DevicePools(data_dev, dataset.dim, params.R)
     fail = pools.init(params.S, params.seed)
     if int(fail.item()):  # pragma: no cover - probability ~ exp(-64)
@@ -495,12 +544,13 @@ def run_rounds(state: BuildState, stats_rows: torch.Tensor | None = None) -> lis
 
 
 def build(dataset: Dataset, params: BuildParams, pair_order: PairOrder = "disordered",
-          report_stats: list | None = None, *, device=None) -> Graph:
+          report_stats: list | None = None, *, device=None, metric: str = "l2") -> Graph:
     """Full build (builder.py:365-390): init, T1 x T2 pair rounds with reverse-edge
     sampling between outer iterations, then graph emission.  One host sync for the
-    init-failure flag, one at the end; every round is a single asynchronous call."""
+    init-failure flag, one at the end; every round is a single asynchronous call.
+    ``metric="ip"`` builds over L2-normalised rows (inner product; not in the reference)."""
     params = effective_params(params, dataset.num_points)
-    state = init_neighbors(dataset, params, pair_order, device=device)
+    state = init_neighbors(dataset, params, pair_order, device=device, metric=metric)
     rows = torch.zeros((num_rounds(params), _lib.NSTATS), dtype=torch.int64, device=state.pools.dev)
     kinds = run_rounds(state, rows)
     graph = finalize_graph(state)
@@ -519,11 +569,17 @@ class DeviceBuild:
     finalize, entirely asynchronous; results stay in HBM."""
 
     def __init__(self, data_dev: torch.Tensor, dim: int, params: BuildParams,
-                 pair_order: PairOrder = "disordered"):
+                 pair_order: PairOrder = "disordered", metric: str = "l2"):
         self.params = effective_params(params, int(data_dev.shape[0]))
         validate_params(self.params, int(data_dev.shape[0]))
+        check_metric(metric)
         self.order = _ORDER_CODES[pair_order]
-        self.pools = _DevicePools(data_dev, dim, self.params.R)
+        self.metric = metric
+        self.raw = data_dev
+        self.dim = dim
+        # IP: every run normalises a copy of the raw vectors (part of the timed build)
+        work = torch.empty_like(data_dev) if metric == "ip" else data_dev
+        self.pools = _DevicePools(work, dim, self.params.R)
         self.rounds = num_rounds(self.params)
         self.stats = torch.zeros((self.rounds, _lib.NSTATS), dtype=torch.int64, device=self.pools.dev)
         self.kinds: list[str] = []
@@ -534,6 +590,10 @@ class DeviceBuild:
         p, pools = self.params, self.pools
         self.stats.zero_()
         self.kinds = []
+        if self.metric == "ip":
+            pools.data.copy_(self.raw)
+            normalize_rows_(pools.data, self.dim)
+        pools.compute_norms()
         fail = pools.init(p.S, p.seed)
         i = 0
         round_index = 0
@@ -554,17 +614,21 @@ class DeviceBuild:
         offsets, nbrs, bad = _finalize_device(pools)
         return offsets, nbrs, bad, fail
 
+    def search_data(self) -> torch.Tensor:
+        """The vectors the graph was built over (normalised rows for IP)."""
+        return self.pools.data
+
     def round_stats(self) -> list[RoundStats]:
         rows = self.stats.cpu().numpy()
         return [RoundStats.from_counters(k, c) for k, c in zip(self.kinds, rows)]
 
 
 def build_fixed_degree(dataset: Dataset, params: BuildParams, pair_order: PairOrder = "disordered",
-                       *, device=None) -> np.ndarray:
+                       *, device=None, metric: str = "l2") -> np.ndarray:
     """Same build, returned as the fixed-degree int32 [N, R] array (rows ascending by
     (dist, id), -1 padded) -- the layout GPU graph builders hand to search kernels."""
     params = effective_params(params, dataset.num_points)
-    state = init_neighbors(dataset, params, pair_order, device=device)
+    state = init_neighbors(dataset, params, pair_order, device=device, metric=metric)
     run_rounds(state)
     return state.fixed_degree()
 

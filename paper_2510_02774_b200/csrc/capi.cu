@@ -88,6 +88,19 @@ __global__ void check_finite_kernel(const float *__restrict__ data, int64_t n, i
     if (__any_sync(FULL, b) && lane_id() == 0) *bad = 1ull;
 }
 
+// end of a round's apply: messages the round could not hold (emit list beyond capacity,
+// or a received message for a row this rank does not own) -> stats[GRNND_ST_LOST]; resets
+// the flags.  The counters are read back with the round's stats (no extra host sync).
+__global__ void lost_kernel(unsigned long long *ctr, int64_t capacity, int64_t *stats) {
+    const unsigned long long m = ctr[C_LIST];
+    unsigned long long lost = m > (unsigned long long)capacity ? m - (unsigned long long)capacity : 0ull;
+    if (ctr[C_OVERFLOW] && !lost) lost = 1ull;
+    if (ctr[C_BADTGT]) lost += 1ull;
+    if (lost && stats) atomicAdd((unsigned long long *)&stats[GRNND_ST_LOST], lost);
+    ctr[C_OVERFLOW] = 0ull;
+    ctr[C_BADTGT] = 0ull;
+}
+
 __global__ void fill_i32_kernel(int32_t *p, int64_t n, int32_t v) {
     const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (x < n) p[x] = v;
@@ -349,7 +362,9 @@ static int apply_phase(const grnnd_pools *p, const Workspace &w, int32_t kind, c
     a.own_after_all = kind == 1 ? 1 : 0;
     a.w = w;
     a.stats = p->stats;
-    return launch_apply_round(a, st);
+    GRNND_TRY(launch_apply_round(a, st));
+    lost_kernel<<<1, 1, 0, st>>>(w.ctr, m_dev ? p->msg_capacity : (int64_t)0x7fffffffffffffffLL, p->stats);
+    return check_launch("lost_kernel");
 }
 
 int grnnd_update_round(const grnnd_pools *p, uint64_t seed, uint64_t stream_id, int32_t order_code,
@@ -417,18 +432,11 @@ int grnnd_round_emit(const grnnd_pools *p, int32_t kind, uint64_t seed, uint64_t
     return launch_bucket_by_rank(w, rank_bounds, nranks, send_counts, S(s));
 }
 
-int grnnd_round_buffers(const grnnd_pools *p, int64_t **out_key, int32_t **out_tgt, int32_t **out_id,
-                        float **out_dist, int64_t **in_key, int32_t **in_tgt, int32_t **in_id, float **in_dist) {
+int grnnd_round_buffers(const grnnd_pools *p, int32_t **out_pack, int32_t **in_pack) {
     Workspace w;
     GRNND_TRY(pools_workspace(p, &w));
-    if (out_key) *out_key = w.o_key;
-    if (out_tgt) *out_tgt = w.o_tgt;
-    if (out_id) *out_id = w.o_id;
-    if (out_dist) *out_dist = w.o_dist;
-    if (in_key) *in_key = w.e_key;
-    if (in_tgt) *in_tgt = w.e_tgt;
-    if (in_id) *in_id = w.e_id;
-    if (in_dist) *in_dist = w.e_dist;
+    if (out_pack) *out_pack = w.o_pack;
+    if (in_pack) *in_pack = w.r_pack;
     return GRNND_OK;
 }
 
@@ -440,6 +448,7 @@ int grnnd_round_apply(const grnnd_pools *p, int32_t kind, int64_t n_incoming, gr
                   (long long)p->msg_capacity);
         return GRNND_EWORKSPACE;
     }
+    GRNND_TRY(launch_unpack(w, n_incoming, p->lo, p->hi - p->lo, S(s)));
     return apply_phase(p, w, kind, nullptr, n_incoming, S(s));
 }
 

@@ -352,8 +352,8 @@ int launch_segsort(const Workspace &w, int64_t n, int64_t *key, int32_t *id, flo
     }
     segsort_medium_kernel<<<sms * 8, MEDIUM_WARPS * 32, 0, st>>>(w.starts, w.heavy, w.ctr + C_HEAVY, key, id, dist);
     GRNND_TRY(check_launch("segsort_medium"));
-    segsort_heavy_kernel<<<sms, HEAVY_T, smem, st>>>(w.starts, w.heavy, w.ctr + C_HEAVY, key, id, dist, w.o_key,
-                                                     w.o_id, w.o_dist);
+    segsort_heavy_kernel<<<sms, HEAVY_T, smem, st>>>(w.starts, w.heavy, w.ctr + C_HEAVY, key, id, dist, w.h_key,
+                                                     w.h_id, w.h_dist);
     return check_launch("segsort_heavy");
 }
 
@@ -454,11 +454,39 @@ __global__ void rank_scatter_kernel(const Workspace w, const int64_t *__restrict
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         const int r = owner_of(w.e_tgt[i], rb, nranks);
         const unsigned long long p = atomicAdd(&cursor[r], 1ull);
-        w.o_key[p] = w.e_key[i];
-        w.o_tgt[p] = w.e_tgt[i];
-        w.o_id[p] = w.e_id[i];
-        w.o_dist[p] = w.e_dist[i];
+        const int64_t key = w.e_key[i];
+        int32_t *o = w.o_pack + p * MSG_WORDS;
+        o[0] = (int32_t)(uint32_t)(uint64_t)key;
+        o[1] = (int32_t)(uint32_t)((uint64_t)key >> 32);
+        o[2] = w.e_tgt[i];
+        o[3] = w.e_id[i];
+        o[4] = __float_as_int(w.e_dist[i]);
     }
+}
+
+// received packed messages (source-rank order) -> the SoA emit list the grouping reads;
+// a target outside the owned range [lo, lo + n) is a protocol error (flagged, dropped)
+__global__ void unpack_kernel(Workspace w, int64_t m, int64_t lo, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t *r = w.r_pack + i * MSG_WORDS;
+        const int64_t key = (int64_t)(((uint64_t)(uint32_t)r[1] << 32) | (uint64_t)(uint32_t)r[0]);
+        int32_t t = r[2];
+        if (t < lo || t >= lo + n) {
+            w.ctr[C_BADTGT] = 1ull;
+            t = (int32_t)lo;  // kept in range; the host raises on the flag
+        }
+        w.e_key[i] = key;
+        w.e_tgt[i] = t;
+        w.e_id[i] = r[3];
+        w.e_dist[i] = __int_as_float(r[4]);
+    }
+}
+
+int launch_unpack(const Workspace &w, int64_t m, int64_t lo, int64_t n, cudaStream_t st) {
+    if (m <= 0) return GRNND_OK;
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)num_sms_cached() * 8));
+    unpack_kernel<<<g, 256, 0, st>>>(w, m, lo, n);
+    return check_launch("unpack_kernel");
 }
 
 int launch_bucket_by_rank(const Workspace &w, const int64_t *rank_bounds, int32_t nranks, int64_t *send_counts,

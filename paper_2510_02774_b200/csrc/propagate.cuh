@@ -65,6 +65,7 @@ int launch_compact(const int32_t *msg_tgt, const int32_t *msg_id, const float *m
                    cudaStream_t st);
 int launch_bucket_by_rank(const Workspace &w, const int64_t *rank_bounds, int32_t nranks,
                           int64_t *send_counts, cudaStream_t st);
+int launch_unpack(const Workspace &w, int64_t m, int64_t lo, int64_t n, cudaStream_t st);
 int launch_scan_counts(const int32_t *counts, int64_t n, int64_t *out, int64_t *tmp,
                        cudaStream_t st);
 int launch_segsort(const Workspace &w, int64_t n, int64_t *key, int32_t *id, float *dist,

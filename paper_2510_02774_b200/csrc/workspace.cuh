@@ -25,6 +25,7 @@ enum Counter : int {
     C_BIN0 = 1,          // C_BIN0 + b: vertices in propagate bin b
     C_HEAVY = C_BIN0 + NBINS,  // segments with > HEAVY_SEG entries
     C_OVERFLOW,          // set when the emit list would exceed msg_capacity
+    C_BADTGT,            // set when a received message targets a row this rank does not own
     C_NCOUNTERS = 16
 };
 
@@ -35,15 +36,19 @@ struct Workspace {
     int32_t *e_tgt;
     int32_t *e_id;
     float *e_dist;
-    // rank-bucketed copy (multi-GPU send buffer) -- also scratch for huge segment sorts
-    int64_t *o_key;
-    int32_t *o_tgt;
-    int32_t *o_id;
-    float *o_dist;
-    // inbox grouped by target row
+    // multi-GPU send buffer: the emit list bucketed by owner rank, packed as MSG_WORDS int32
+    // per message (key lo, key hi, tgt, id, dist bits) so one all-to-all moves it.  Outside
+    // the exchange it is scratch for huge segment sorts (h_key / h_id / h_dist alias it).
+    int32_t *o_pack;
+    int64_t *h_key;
+    int32_t *h_id;
+    float *h_dist;
+    // inbox grouped by target row; before grouping the same bytes receive the packed
+    // messages of the exchange (r_pack)
     int64_t *i_key;
     int32_t *i_id;
     float *i_dist;
+    int32_t *r_pack;
     int32_t *in_count;   // [n+1] per-target counts (self-resetting)
     int64_t *starts;     // [n+1]
     int64_t *scan_tmp;   // [scan blocks + 1]
@@ -68,6 +73,7 @@ struct Workspace {
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 constexpr int SCAN_ITEMS = 2048;  // elements per scan block
+constexpr int MSG_WORDS = 5;       // packed message: int64 key, int32 tgt, int32 id, fp32 dist
 
 inline int64_t scan_blocks(int64_t n) { return (n + SCAN_ITEMS - 1) / SCAN_ITEMS; }
 
@@ -88,13 +94,17 @@ inline size_t carve(Workspace *w, void *base, int64_t n, int32_t cap, int64_t ms
     t.e_tgt = (int32_t *)take(4 * C);
     t.e_id = (int32_t *)take(4 * C);
     t.e_dist = (float *)take(4 * C);
-    t.o_key = (int64_t *)take(8 * C);
-    t.o_tgt = (int32_t *)take(4 * C);
-    t.o_id = (int32_t *)take(4 * C);
-    t.o_dist = (float *)take(4 * C);
-    t.i_key = (int64_t *)take(8 * C);
-    t.i_id = (int32_t *)take(4 * C);
-    t.i_dist = (float *)take(4 * C);
+    t.o_pack = (int32_t *)take(4 * MSG_WORDS * C);
+    t.h_key = (int64_t *)t.o_pack;
+    t.h_id = t.o_pack ? (int32_t *)((char *)t.o_pack + 8 * C) : nullptr;
+    t.h_dist = t.o_pack ? (float *)((char *)t.o_pack + 12 * C) : nullptr;
+    {
+        char *ib = (char *)take(4 * MSG_WORDS * C);  // >= the 16 C bytes of the inbox
+        t.r_pack = (int32_t *)ib;
+        t.i_key = (int64_t *)ib;
+        t.i_id = ib ? (int32_t *)(ib + 8 * C) : nullptr;
+        t.i_dist = ib ? (float *)(ib + 12 * C) : nullptr;
+    }
     t.in_count = (int32_t *)take(4 * (N + 1));
     t.starts = (int64_t *)take(8 * (N + 1));
     t.scan_tmp = (int64_t *)take(8 * (size_t)(scan_blocks((int64_t)N) + 2 + 128));

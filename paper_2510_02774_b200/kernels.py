@@ -11,8 +11,8 @@ sm_100a kernel through the C ABI, and copies the results back; it is the
 parity surface, not the fast path (``paper_2510_02774_b200.build`` keeps the
 pools resident in HBM instead).
 
-Evaluation kernels (brute_force, greedy_search_*, refine_accept_loop) are out
-of scope for this build-path drop-in and raise NotImplementedError.
+The evaluation kernels brute_force / greedy_search_* run csrc/search.cu;
+refine_accept_loop (the sequential oracle's loop) raises NotImplementedError.
 """
 
 from __future__ import annotations
@@ -211,20 +211,53 @@ def warmup() -> None:
     sqdist(data[0], data[1])
 
 
-def _out_of_scope(name):
-    def f(*a, **k):
-        raise NotImplementedError(f"{name} is an evaluation kernel, outside the B200 build-path drop-in")
-    f.__name__ = name
-    return f
+def brute_force(data, queries, k, out_ids):
+    """_numba_kernels.brute_force (:384-413): exact k nearest ids per query (ties by id),
+    written into ``out_ids`` int32 [nq, k] in place."""
+    from .search import brute_force_device
+
+    dev = _dev()
+    data = np.asarray(data, dtype=np.float32)
+    q = np.asarray(queries, dtype=np.float32).reshape(-1, data.shape[1])
+    ids = brute_force_device(upload(data, dev), data.shape[1], upload(q, dev), int(k))
+    out_ids[...] = ids.cpu().numpy()
 
 
-brute_force = _out_of_scope("brute_force")
-greedy_search_single = _out_of_scope("greedy_search_single")
-greedy_search_batch = _out_of_scope("greedy_search_batch")
-refine_accept_loop = _out_of_scope("refine_accept_loop")
+def _greedy(offsets, nbrs, data, queries, L, k, entries):
+    from .search import search_device
+
+    dev = _dev()
+    data = np.asarray(data, dtype=np.float32)
+    q = np.asarray(queries, dtype=np.float32).reshape(-1, data.shape[1])
+    off = _to(offsets, np.int64)
+    nb = _to(nbrs if len(nbrs) else np.zeros(1, np.int32), np.int32)
+    ent = _to(np.asarray(entries, dtype=np.int64).reshape(-1), np.int64)
+    ids, d, cnt = search_device(off, nb, upload(data, dev), data.shape[1], upload(q, dev), int(L), int(k), ent,
+                                with_dists=True)
+    return ids.cpu().numpy(), d.cpu().numpy(), cnt.cpu().numpy()
+
+
+def greedy_search_single(offsets, nbrs, data, q, L, k, entry):
+    """_numba_kernels.greedy_search_single (:466-477): (ids[:cnt], dists[:cnt])."""
+    ids, d, cnt = _greedy(offsets, nbrs, data, np.asarray(q).reshape(1, -1), L, k, [int(entry)])
+    c = int(cnt[0])
+    return ids[0, :c], d[0, :c]
+
+
+def greedy_search_batch(offsets, nbrs, data, queries, L, k, entries):
+    """_numba_kernels.greedy_search_batch (:503-513): (out_ids, out_d, out_cnt)."""
+    return _greedy(offsets, nbrs, data, queries, L, k, entries)
+
+
+def refine_accept_loop(*a, **k):
+    """The sequential RNN-Descent oracle's inner loop (_numba_kernels.py:354-381) belongs to
+    build_seq, which is not part of the parallel build path."""
+    raise NotImplementedError("refine_accept_loop (sequential oracle) is not on the B200 build path")
+
 
 __all__ = [
     "hash4_u64", "sqdist", "sample_initial", "init_dists", "gen_update_messages", "gen_reverse_messages",
     "gen_merge_messages", "build_flat", "group_by_target", "apply_grouped_messages", "warmup",
+    "brute_force", "greedy_search_single", "greedy_search_batch",
     "padded_ld",
 ]

@@ -1,0 +1,140 @@
+"""GPU evaluation kernels (csrc/search.cu) and reference-pinned whole-build digests.
+
+Bar: bit-exact.  Brute force and greedy search use the reference's exact fp32 distance
+and (dist, id) order, so ids must equal the reference's (numba) ids -- checked against
+fixtures the reference produced (tests/golden/make_reference_digest.py, make_golden.py)
+and against the pinned CPU oracle.
+"""
+
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+
+from paper_2510_02774_b200.core import generate  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def g():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2510_02774_b200 as pkg
+
+    return pkg
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def c1(g, golden):
+    """BASELINE config 1 built on the GPU (20K x 128 gaussian, S20 R96 T1=4 T2=15)."""
+    ref = golden("c1_reference")
+    meta = json.loads(str(ref["meta"]))
+    ds = generate(meta["n"], meta["dim"], "gaussian", seed=1)
+    log = []
+    graph = g.build(ds, g.BuildParams(S=20, R=96, T1=4, T2=15, rho=0.6, seed=1), report_stats=log)
+    return ds, graph, log, ref, meta
+
+
+def test_c1_graph_equals_reference_digest(c1):
+    """The GPU graph's bytes hash to the digest of the reference's own numba build."""
+    ds, graph, log, ref, meta = c1
+    assert sha(graph.offsets.astype(np.int64)) == meta["sha256_offsets"]
+    assert sha(graph.neighbor_ids.astype(np.int32)) == meta["sha256_neighbor_ids"]
+    stats = np.array([[s.messages, s.redirects, s.survivors, s.reverse_attempts, s.inserted, s.duplicate,
+                       s.replaced, s.rejected] for s in log], np.int64)
+    assert np.array_equal(stats, ref["stats"])
+
+
+def test_c1_search_and_truth_equal_reference(g, c1):
+    """search_batch at L in {32..256} and brute-force truth: the reference's ids exactly."""
+    ds, graph, _, ref, meta = c1
+    q = generate(1000, ds.dim, "gaussian", seed=2).data
+    truth = g.brute_force_knn_batch(ds, q, 10)
+    assert np.array_equal(truth, ref["truth"])
+    for li, L in enumerate(ref["Ls"].tolist()):
+        ids, secs = g.search_batch(graph, ds, q, g.SearchParams(L=L, k=10))
+        assert np.array_equal(ids, ref["search_ids"][li]), L
+        assert g.mean_recall(ids, truth) == pytest.approx(float(ref["recall"][li]), abs=1e-12)
+        assert secs > 0
+
+
+def test_c1_knn_graph_recall_equals_reference(g, c1):
+    ds, graph, _, ref, _ = c1
+    sample = ref["knn_sample"]
+    t11 = g.brute_force_knn_batch(ds, ds.data[sample], 11)
+    t10 = np.array([[x for x in row if x != v][:10] for row, v in zip(t11, sample)], np.int32)
+    assert np.array_equal(t10, ref["knn_truth"])
+    from paper_2510_02774_b200.search import knn_graph_recall
+
+    assert knn_graph_recall(graph, t10, sample) == pytest.approx(float(ref["knn_graph_recall"]), abs=1e-12)
+
+
+def test_acceptance_corpus_search_ids(g, golden):
+    """criterion 03 (test_acceptance.py): the reference's search ids at L=64, k=10."""
+    a = golden("acceptance10k")
+    ds = generate(10000, 16, "uniform", seed=1)
+    graph = g.Graph(10000, a["offsets"], a["nbrs"], 32)
+    q = generate(100, 16, "uniform", seed=2).data
+    ids, _ = g.search_batch(graph, ds, q, g.SearchParams(L=64, k=10))
+    assert np.array_equal(ids, a["search_ids"])
+    assert np.array_equal(g.brute_force_knn_batch(ds, q, 10), a["truth"])
+    assert g.mean_recall(ids, a["truth"]) == pytest.approx(0.9770, abs=1e-12)
+
+
+@pytest.mark.parametrize("n,dim,dist,L,k", [(3000, 3, "uniform", 16, 5), (5000, 24, "clustered", 100, 10),
+                                            (2000, 960, "gaussian", 40, 20), (4000, 1, "uniform", 8, 8)])
+def test_search_and_brute_force_vs_oracle(g, n, dim, dist, L, k):
+    """Against the oracle: ragged ld padding, D=960, D=1 (massive distance ties: the id
+    tie rule decides), random entries (SearchParams(entry=None))."""
+    ds = generate(n, dim, dist, seed=7)
+    graph = g.build(ds, g.BuildParams(S=8, R=24, T1=2, T2=3, seed=7))
+    q = generate(64, dim, dist, seed=8).data
+    assert np.array_equal(g.brute_force_knn_batch(ds, q, k), oracle.brute_force_knn(ds.data, q, k))
+    ids, _ = g.search_batch(graph, ds, q, g.SearchParams(L=L, k=k))
+    assert np.array_equal(ids, oracle.greedy_search(graph.offsets, graph.neighbor_ids, ds.data, q, L, k))
+    sp = g.SearchParams(L=L, k=k, entry=None, seed=5)
+    from paper_2510_02774_b200.search import _entries_for
+
+    ent = _entries_for(sp, n, q.shape[0])
+    ids, _ = g.search_batch(graph, ds, q, sp)
+    assert np.array_equal(ids, oracle.greedy_search(graph.offsets, graph.neighbor_ids, ds.data, q, L, k, ent))
+
+
+def test_search_edges_and_kernel_module(g):
+    from paper_2510_02774_b200 import kernels as K
+
+    ds = generate(500, 8, "uniform", seed=3)
+    # a graph with isolated vertices: fewer than k reachable -> -1 padding
+    off = np.zeros(501, np.int64)
+    off[1:] = np.minimum(np.arange(1, 501), 3)  # vertex 0 -> 1, 1 -> 2, 2 -> 0; all others empty
+    nb = np.array([1, 2, 0], np.int32)
+    graph = g.Graph(500, off, nb)
+    q = ds.data[:4]
+    ids, _ = g.search_batch(graph, ds, q, g.SearchParams(L=8, k=5))
+    want = oracle.greedy_search(off, nb, ds.data, q, 8, 5)
+    assert np.array_equal(ids, want) and np.all(ids[:, 3:] == -1)
+    one = g.greedy_search(graph, ds, q[0], g.SearchParams(L=8, k=5))
+    assert np.array_equal(one, want[0, :3])
+    i1, d1 = K.greedy_search_single(off, nb, ds.data, q[1], 8, 5, 0)
+    assert np.array_equal(i1, want[1, :3]) and d1.dtype == np.float32 and np.all(np.diff(d1) >= 0)
+    out = np.empty((4, 6), np.int32)
+    K.brute_force(ds.data, q, 6, out)
+    assert np.array_equal(out, oracle.brute_force_knn(ds.data, q, 6))
+    assert np.array_equal(g.brute_force_knn(ds, q[0], 3), out[0, :3])
+    with pytest.raises(g.ParamError):
+        g.search_batch(graph, ds, q, g.SearchParams(L=4, k=5))
+    with pytest.raises(g.DimensionMismatch):
+        g.search_batch(graph, ds, q[:, :3], g.SearchParams(L=8, k=5))
+    with pytest.raises(g.EmptyGraph):
+        g.search_batch(g.Graph(0, np.zeros(1, np.int64), np.zeros(0, np.int32)), ds, q, g.SearchParams(L=8, k=5))
+    with pytest.raises(g.ParamError):
+        g.brute_force_knn_batch(ds, q, 501)

@@ -19,7 +19,7 @@ import torch.multiprocessing as mp
 
 import oracle
 from paper_2510_02774_b200.core import generate
-from paper_2510_02774_b200.sharded import FIELDS, exchange_all_to_all, shard_bounds
+from paper_2510_02774_b200.sharded import MSG_WORDS, exchange_all_to_all, pack_messages, shard_bounds, unpack_messages
 
 
 def _free_port():
@@ -89,14 +89,14 @@ def _worker(rank, world, port, cfg, out_q):
                 order = np.argsort(owner, kind="stable") if msgs else []
                 msgs = [msgs[i] for i in order]
                 send_counts = [int(np.sum(np.asarray(owner) == r)) for r in range(world)]
-                cap = max(sum(send_counts), 1)
-                out = {"key": torch.tensor([m[0] for m in msgs] + [0] * (cap - len(msgs)), dtype=torch.int64),
-                       "tgt": torch.tensor([m[1] for m in msgs] + [0] * (cap - len(msgs)), dtype=torch.int32),
-                       "id": torch.tensor([m[2] for m in msgs] + [0] * (cap - len(msgs)), dtype=torch.int32),
-                       "dist": torch.tensor([m[3] for m in msgs] + [0] * (cap - len(msgs)), dtype=torch.float32)}
-                inb = {f: torch.zeros(n * R, dtype=dt) for f, dt in FIELDS}
+                # the packed payload (one all-to-all per round), as rank_scatter_kernel lays it out
+                out = pack_messages(torch.tensor([m[0] for m in msgs], dtype=torch.int64),
+                                    torch.tensor([m[1] for m in msgs], dtype=torch.int32),
+                                    torch.tensor([m[2] for m in msgs], dtype=torch.int32),
+                                    torch.tensor([m[3] for m in msgs], dtype=torch.float32))
+                inb = torch.zeros((n * R, MSG_WORDS), dtype=torch.int32)
                 n_in = exchange_all_to_all(out, send_counts, inb)
-                incoming = tuple(inb[f][:n_in].numpy() for f, _ in FIELDS)
+                incoming = tuple(x.numpy() for x in unpack_messages(inb[:n_in]))
                 rid, rd, rc = _apply_ordered(rows, R, lo, kind, incoming, rid, rd, rc)
         off, nb = oracle.finalize(rid, rd, rc)
         parts = [None] * world
@@ -132,6 +132,16 @@ def test_sharded_exchange_cpu_gloo_bit_exact(world):
     assert np.array_equal(np.concatenate(nbrs), want_nb)
 
 
+def test_pack_roundtrip():
+    key = torch.tensor([0, 1, 2**40 + 5, 9_600_000_000, 2**31 - 1, 2**32 + 7], dtype=torch.int64)
+    tgt = torch.arange(6, dtype=torch.int32)
+    mid = torch.arange(6, dtype=torch.int32) * 3
+    d = torch.tensor([0.0, 1.5, float("inf"), 3e-38, 7.25, -0.0], dtype=torch.float32)
+    k2, t2, i2, d2 = unpack_messages(pack_messages(key, tgt, mid, d))
+    assert torch.equal(k2, key) and torch.equal(t2, tgt) and torch.equal(i2, mid)
+    assert torch.equal(d2.view(torch.int32), d.view(torch.int32))
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [2, 3, 4])
 def test_virtual_shards_bit_exact(world):
@@ -150,3 +160,41 @@ def test_virtual_shards_bit_exact(world):
     assert [s.inserted for s in logp] == [s.inserted for s in log1]
     off, nb = oracle.build(ds.data, 12, 32, 3, 3, 0.6, 4)
     assert np.array_equal(shard.neighbor_ids, nb)
+
+
+@pytest.mark.gpu
+def test_virtual_shards_hub_and_ip():
+    """A hub (many vertices near one point: segments above the bitonic cap, the heavy sort
+    that uses the send buffer as scratch) and the IP metric through the sharded driver."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2510_02774_b200 as g
+    from paper_2510_02774_b200.sharded import build_virtual_shards
+
+    r = np.random.default_rng(11)
+    x = np.concatenate([r.standard_normal((200, 16)) * 0.001, r.standard_normal((9800, 16))]).astype(np.float32)
+    ds = g.Dataset(x)
+    params = g.BuildParams(S=16, R=64, T1=2, T2=3, rho=1.0, seed=2)
+    one = g.build(ds, params)
+    for world in (2, 4):
+        sh = build_virtual_shards(ds, params, world)
+        assert np.array_equal(sh.offsets, one.offsets) and np.array_equal(sh.neighbor_ids, one.neighbor_ids)
+    ip1 = g.build(ds, params, metric="ip")
+    ip2 = build_virtual_shards(ds, params, 3, metric="ip")
+    assert np.array_equal(ip1.offsets, ip2.offsets) and np.array_equal(ip1.neighbor_ids, ip2.neighbor_ids)
+    off, nb = oracle.build(oracle.normalize_rows(x), 16, 64, 2, 3, 1.0, 2)
+    assert np.array_equal(ip1.offsets, off) and np.array_equal(ip1.neighbor_ids, nb)
+
+
+@pytest.mark.gpu
+def test_message_overflow_is_reported():
+    """A message capacity below what a round emits is reported (DeviceError), never a
+    silently wrong graph."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2510_02774_b200 as g
+    from paper_2510_02774_b200.sharded import build_virtual_shards
+
+    ds = generate(3000, 16, "gaussian", seed=1)
+    with pytest.raises(g.DeviceError):
+        build_virtual_shards(ds, g.BuildParams(S=16, R=32, T1=2, T2=2, seed=1), 2, msg_capacity=2000)
