@@ -403,6 +403,9 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
                            "pairs_per_round": int(sum(pairs_all) / len(pairs_all)),
                            "pairs_ref_per_round": int(sum(pairs_ref) / len(pairs_ref)),
                            "exact_reevaluated_frac": round(sum(cands) / max(sum(pairs_all), 1), 5),
+                           "redirectable_pairs_per_round": int(sum(s.redirectable for s in upd) / len(upd)),
+                           "pools_with_redirectable_pairs_frac": round(
+                               sum(s.record_pools for s in upd) / (len(upd) * args.n), 4),
                            "sm_mhz": sm_mhz},
             "phase_ms_per_round": {"propagate": round(sum(prop_ms) / len(prop_ms), 3),
                                    "group_apply": round(sum(apply_ms) / len(apply_ms), 3)},

@@ -60,10 +60,16 @@ enum {
     GRNND_ST_CANDIDATES = 10, /* pairs the filtered pair phase re-evaluated exactly (instrumentation) */
     GRNND_ST_OVERFLOWS = 11,  /* groups whose candidate queue overflowed into an exact sweep */
     GRNND_ST_REDIRECTABLE = 12, /* pairs meeting the redirect condition (instrumentation)      */
+    GRNND_ST_RECPOOLS = 14,   /* pools with at least one redirect-capable pair (instrumentation) */
     GRNND_ST_LOST = 13,       /* messages a round could not hold (emit list beyond msg_capacity)
                                  or that reached the wrong rank: non-zero = the round is invalid,
                                  the Python layer raises DeviceError (GRNND_EWORKSPACE meaning) */
-    GRNND_NSTATS = 16
+    /* validation builds only (-DGRNND_TC_VALIDATE, libgrnnd_b200_tcv.so): the tensor-core
+       pre-screen's error against its rigorous bound, checked on every screened pair */
+    GRNND_ST_TCV_CHECKED = 16,    /* pairs whose screened distance was compared with the exact one */
+    GRNND_ST_TCV_MAX_RATIO = 17,  /* max |d~ - d| / bound, fp32 bits (ratio >= 0)                  */
+    GRNND_ST_TCV_VIOLATIONS = 18, /* pairs with |d~ - d| > bound (must stay 0)                     */
+    GRNND_NSTATS = 20
 };
 
 typedef void *grnnd_stream_t; /* a cudaStream_t */

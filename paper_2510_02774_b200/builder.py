@@ -88,6 +88,8 @@ class RoundStats:
     pairs: int = field(default=0, compare=False, repr=False)
     pairs_ref: int = field(default=0, compare=False, repr=False)
     candidates: int = field(default=0, compare=False, repr=False)  # filter band re-evaluations
+    redirectable: int = field(default=0, compare=False, repr=False)  # pairs meeting the redirect condition
+    record_pools: int = field(default=0, compare=False, repr=False)  # pools with >= 1 such pair
 
     @classmethod
     def from_counters(cls, kind: str, c) -> "RoundStats":
@@ -108,6 +110,8 @@ class RoundStats:
             pairs=c[_lib.ST_PAIRS],
             pairs_ref=c[_lib.ST_PAIRS_REF],
             candidates=c[_lib.ST_CANDIDATES],
+            redirectable=c[_lib.ST_REDIRECTABLE],
+            record_pools=c[_lib.ST_RECPOOLS],
         )
         if kind == "update":
             st.survivors = st.messages - st.redirects
@@ -241,6 +245,7 @@ class _DevicePools:
         ws = int(_lib.lib.grnnd_workspace_bytes(rows, cap, self.msg_capacity))
         self.workspace = torch.zeros(ws, dtype=torch.uint8, device=dev)
         self.scratch_stats = torch.zeros(_lib.NSTATS, dtype=torch.int64, device=dev)
+        self.version = 0  # bumped on every state change (host snapshot cache key)
         # filtered pair phase (FFMA dot pre-screen + exact re-evaluation near the threshold;
         # same graph as the exact-only phase): needs the squared norms of every row
         if filtered is None:
@@ -284,6 +289,7 @@ class _DevicePools:
         self.read_dists, self.write_dists = self.write_dists, self.read_dists
         self.read_count, self.write_count = self.write_count, self.read_count
         self.write_count.zero_()
+        self.version += 1
 
     # -- the four asynchronous steps --
     @_on_device
@@ -291,6 +297,7 @@ class _DevicePools:
         fail = torch.zeros(1, dtype=torch.int64, device=self.dev)
         p = self.struct()
         _lib.call("grnnd_init_pools", C.byref(p), S, seed & MASK64, fail.data_ptr(), _stream(self.dev))
+        self.version += 1
         return fail
 
     @_on_device
@@ -343,19 +350,52 @@ class _DevicePools:
 class BuildState:
     """Device-resident twin of builder.BuildState (builder.py:117-176).
 
-    ``read_ids`` / ``read_dists`` / ``read_count`` / ``write_*`` are host
-    snapshots (numpy copies; slots beyond a row's count read as TOMBSTONE /
-    inf like the reference's cleared buffers); the live tensors are
+    Two constructors: the internal one (``BuildState(dataset, params, pools)``) and the
+    reference's keyword form ``BuildState(data=..., params=..., read_ids=..., read_dists=...,
+    read_count=..., write_ids=..., write_dists=..., write_count=..., round_index=0,
+    pair_order="disordered")`` (test_builder.py:89), which uploads the arrays.
+
+    ``read_ids`` / ``read_dists`` / ``read_count`` / ``write_*`` are READ-ONLY host
+    snapshots (numpy, ``writeable=False``; slots beyond a row's count read as TOMBSTONE /
+    inf like the reference's cleared buffers), cached until the next round or swap: one
+    device-to-host copy per state change, not per access.  The live tensors are
     ``state.pools.read_ids`` etc.
     """
 
-    def __init__(self, dataset: Dataset, params: BuildParams, pools: _DevicePools, pair_order: str = "disordered"):
+    def __init__(self, dataset=None, params: BuildParams | None = None, pools: "_DevicePools | None" = None,
+                 pair_order: str = "disordered", *, data=None, read_ids=None, read_dists=None, read_count=None,
+                 write_ids=None, write_dists=None, write_count=None, round_index: int = 0, totals=None,
+                 device=None):
+        if pools is None:
+            if data is None and dataset is not None:
+                data = dataset.data if isinstance(dataset, Dataset) else dataset
+            if data is None or read_ids is None or read_dists is None or read_count is None:
+                raise ParamError("BuildState needs (dataset, params, pools) or data= and the read_* arrays")
+            ds = data if isinstance(data, Dataset) else Dataset(data)
+            ri = np.ascontiguousarray(read_ids, dtype=np.int32)
+            n, cap = ri.shape
+            dev = _device(device)
+            with torch.cuda.device(dev):
+                pools = _DevicePools(upload(ds.data, dev), ds.dim, cap)
+                pools.read_ids.copy_(torch.from_numpy(ri))
+                pools.read_dists.copy_(torch.from_numpy(np.ascontiguousarray(read_dists, dtype=np.float32)))
+                pools.read_count.copy_(torch.from_numpy(np.ascontiguousarray(read_count, dtype=np.int32)))
+                if write_count is not None:
+                    wc = np.ascontiguousarray(write_count, dtype=np.int32)
+                    pools.write_count.copy_(torch.from_numpy(wc))
+                    if write_ids is not None:
+                        pools.write_ids.copy_(torch.from_numpy(np.ascontiguousarray(write_ids, dtype=np.int32)))
+                    if write_dists is not None:
+                        pools.write_dists.copy_(torch.from_numpy(np.ascontiguousarray(write_dists, dtype=np.float32)))
+            dataset = ds
         self.dataset = dataset
         self.params = params
         self.pools = pools
         self.pair_order = pair_order
-        self.round_index = 0
-        self.totals = RoundStats(kind="total")
+        self.round_index = round_index
+        self.totals = totals if totals is not None else RoundStats(kind="total")
+        self._snap: dict = {}
+        self._snap_version = -1
 
     # --- shape ---
     @property
@@ -370,7 +410,21 @@ class BuildState:
     def data(self) -> np.ndarray:
         return self.dataset.data
 
-    # --- host snapshots ---
+    # --- host snapshots (read-only, cached per pool version) ---
+    def _cached(self, side: str):
+        if self._snap_version != self.pools.version:
+            self._snap = {}
+            self._snap_version = self.pools.version
+        if side not in self._snap:
+            P = self.pools
+            ids, dists, counts = ((P.read_ids, P.read_dists, P.read_count) if side == "read"
+                                  else (P.write_ids, P.write_dists, P.write_count))
+            out = self._masked(ids, dists, counts)
+            for a in out:
+                a.setflags(write=False)
+            self._snap[side] = out
+        return self._snap[side]
+
     def _masked(self, ids: torch.Tensor, dists: torch.Tensor, counts: torch.Tensor):
         c = counts.cpu().numpy().astype(np.int32)
         i = ids.cpu().numpy()
@@ -380,35 +434,35 @@ class BuildState:
 
     @property
     def read_ids(self) -> np.ndarray:
-        return self._masked(self.pools.read_ids, self.pools.read_dists, self.pools.read_count)[0]
+        return self._cached("read")[0]
 
     @property
     def read_dists(self) -> np.ndarray:
-        return self._masked(self.pools.read_ids, self.pools.read_dists, self.pools.read_count)[1]
+        return self._cached("read")[1]
 
     @property
     def read_count(self) -> np.ndarray:
-        return self.pools.read_count.cpu().numpy().astype(np.int32)
+        return self._cached("read")[2]
 
     @property
     def write_ids(self) -> np.ndarray:
-        return self._masked(self.pools.write_ids, self.pools.write_dists, self.pools.write_count)[0]
+        return self._cached("write")[0]
 
     @property
     def write_dists(self) -> np.ndarray:
-        return self._masked(self.pools.write_ids, self.pools.write_dists, self.pools.write_count)[1]
+        return self._cached("write")[1]
 
     @property
     def write_count(self) -> np.ndarray:
-        return self.pools.write_count.cpu().numpy().astype(np.int32)
+        return self._cached("write")[2]
 
     def snapshot(self):
-        """(read_ids, read_dists, read_count) host copies in one transfer."""
-        return self._masked(self.pools.read_ids, self.pools.read_dists, self.pools.read_count)
+        """(read_ids, read_dists, read_count) host copies (read-only)."""
+        return self._cached("read")
 
     def pool(self, v: int) -> DoubleBufferPool:
         ri, rd, _ = self.snapshot()
-        wi, wd, wc = self._masked(self.pools.write_ids, self.pools.write_dists, self.pools.write_count)
+        wi, wd, wc = self._cached("write")
         return DoubleBufferPool(owner=v, read_ids=ri[v], read_dists=rd[v], write_ids=wi[v],
                                 write_dists=wd[v], write_count=int(wc[v]))
 
@@ -423,15 +477,8 @@ class BuildState:
     def from_arrays(cls, data, params: BuildParams, read_ids, read_dists, read_count,
                     pair_order: str = "disordered", device=None) -> "BuildState":
         """A state with caller-set read pools (the reference tests' _manual_state)."""
-        dev = _device(device)
-        ds = Dataset(data)
-        ri = np.ascontiguousarray(read_ids, dtype=np.int32)
-        n, cap = ri.shape
-        pools = _DevicePools(upload(ds.data, dev), ds.dim, cap)
-        pools.read_ids.copy_(torch.from_numpy(ri))
-        pools.read_dists.copy_(torch.from_numpy(np.ascontiguousarray(read_dists, dtype=np.float32)))
-        pools.read_count.copy_(torch.from_numpy(np.ascontiguousarray(read_count, dtype=np.int32)))
-        return cls(ds, params, pools, pair_order)
+        return cls(params=params, data=data, read_ids=read_ids, read_dists=read_dists, read_count=read_count,
+                   pair_order=pair_order, device=device)
 
 
 def init_neighbors(dataset: Dataset, params: BuildParams, pair_order: PairOrder = "disordered",
@@ -638,8 +685,9 @@ def validate_state(state: BuildState, tol: float = 1e-4) -> None:
     n, cap = state.num_vertices, state.capacity
     ids, dists, counts = state.snapshot()
     assert counts.min() >= 0 and counts.max() <= cap, "read count out of range"
+    # the device write buffer is cleared logically (count 0; slots beyond a row's count are
+    # never read), so "empty" is exactly a zero count (the reference's TOMB fill, :402-404)
     assert np.all(state.write_count == 0), "write buffers not empty at boundary"
-    assert np.all(state.write_ids == TOMBSTONE), "write buffer has stale entries"
     valid = np.arange(cap)[None, :] < counts[:, None]
     assert np.all(ids[valid] >= 0), "tombstone inside the packed prefix"
     assert np.all(ids[~valid] == TOMBSTONE), "valid id beyond the packed prefix"

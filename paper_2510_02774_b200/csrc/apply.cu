@@ -336,21 +336,11 @@ __global__ void __launch_bounds__(256) apply_grouped_kernel(int32_t *__restrict_
     }
 }
 
-static int sms_for_apply() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
-}
 
 
 int launch_apply_round(const ApplyArgs &a, cudaStream_t st) {
     if (a.n <= 0) return GRNND_OK;
-    const int64_t blocks = std::min<int64_t>((a.n + 7) / 8, (int64_t)sms_for_apply() * 8);
+    const int64_t blocks = std::min<int64_t>((a.n + 7) / 8, (int64_t)device_sm_count() * 8);
     const unsigned g = (unsigned)std::max<int64_t>(1, blocks);
     switch ((a.cap + 31) / 32) {
         case 1: apply_round_kernel<1><<<g, 256, 0, st>>>(a); break;
@@ -370,7 +360,7 @@ int launch_apply_grouped(int32_t *write_ids, float *write_dists, int32_t *write_
                          const int32_t *flat_id, const float *flat_dist, const int64_t *order, const int64_t *starts,
                          int64_t *outcomes, cudaStream_t st) {
     if (n <= 0) return GRNND_OK;
-    const int64_t blocks = std::min<int64_t>((n + 7) / 8, (int64_t)sms_for_apply() * 8);
+    const int64_t blocks = std::min<int64_t>((n + 7) / 8, (int64_t)device_sm_count() * 8);
     const unsigned g = (unsigned)std::max<int64_t>(1, blocks);
     unsigned long long *oc = (unsigned long long *)outcomes;
     switch ((cap + 31) / 32) {

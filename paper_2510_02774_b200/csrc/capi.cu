@@ -21,6 +21,24 @@ static unsigned long long g_launches = 0;  // kernels this library launched (hos
 
 unsigned long long launch_count() { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
 
+int current_device() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) return 0;
+    return d;
+}
+
+int device_sm_count() {
+    static int cache[MAX_DEVICES] = {0};
+    const int d = current_device();
+    const int slot = d >= 0 && d < MAX_DEVICES ? d : 0;
+    int s = __atomic_load_n(&cache[slot], __ATOMIC_RELAXED);
+    if (!s) {
+        if (cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || s <= 0) s = 148;
+        __atomic_store_n(&cache[slot], s, __ATOMIC_RELAXED);
+    }
+    return s;
+}
+
 int check_launch(const char *what, int nkernels) {
     __atomic_fetch_add(&g_launches, (unsigned long long)nkernels, __ATOMIC_RELAXED);
     cudaError_t e = cudaGetLastError();

@@ -83,11 +83,29 @@ __device__ __forceinline__ T warp_sum(T v) {
 
 }  // namespace grnnd
 
-// ---- host-side error plumbing (capi.cu) ----
+// ---- host-side error plumbing and per-device launch state (capi.cu) ----
 namespace grnnd {
 void set_error(const char* fmt, ...);
 int check_launch(const char* what, int nkernels = 1);
 unsigned long long launch_count();
+constexpr int MAX_DEVICES = 64;
+// SM count of the CUDA runtime's current device (cached per device)
+int device_sm_count();
+int current_device();
+// Dynamic shared memory opt-in of one kernel, remembered per device: the attribute is set
+// on the first launch on each device (and again if a launch needs more).
+struct SmemOptIn {
+    int bytes[MAX_DEVICES] = {0};
+    template <class K>
+    cudaError_t ensure(K kern, size_t smem) {
+        const int d = current_device();
+        if (d < 0 || d >= MAX_DEVICES) return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if ((int)smem <= bytes[d]) return cudaSuccess;
+        const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) bytes[d] = (int)smem;
+        return e;
+    }
+};
 }  // namespace grnnd
 
 #define GRNND_TRY(expr)                        \

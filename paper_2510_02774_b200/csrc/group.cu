@@ -327,29 +327,16 @@ __global__ void __launch_bounds__(HEAVY_T) segsort_heavy_kernel(const int64_t *_
     }
 }
 
-static int num_sms_cached() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
-    return sms;
-}
 
 int launch_segsort(const Workspace &w, int64_t n, int64_t *key, int32_t *id, float *dist, cudaStream_t st) {
-    const int sms = num_sms_cached();
+    const int sms = device_sm_count();
     const int64_t warps_needed = (n + 31) / 32;
     const int64_t blocks = std::min<int64_t>((warps_needed + 7) / 8, (int64_t)sms * 16);
     segsort_light_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(w.starts, n, key, id, dist);
     GRNND_TRY(check_launch("segsort_light"));
     const size_t smem = (size_t)HEAVY_CAP * (8 + 4 + 4 + 2);
-    static bool configured = false;
-    if (!configured) {
-        GRNND_CUDA(cudaFuncSetAttribute(segsort_heavy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = true;
-    }
+    static SmemOptIn optin;
+    GRNND_CUDA(optin.ensure(segsort_heavy_kernel, smem));
     segsort_medium_kernel<<<sms * 8, MEDIUM_WARPS * 32, 0, st>>>(w.starts, w.heavy, w.ctr + C_HEAVY, key, id, dist);
     GRNND_TRY(check_launch("segsort_medium"));
     segsort_heavy_kernel<<<sms, HEAVY_T, smem, st>>>(w.starts, w.heavy, w.ctr + C_HEAVY, key, id, dist, w.h_key,
@@ -363,7 +350,7 @@ int launch_group_inbox(const Workspace &w, const int64_t *key, const int32_t *tg
                        const float *dist, const unsigned long long *m_dev, int64_t m_host, int64_t lo, int64_t n,
                        cudaStream_t st) {
     const int64_t m = m_host;
-    const int sms = num_sms_cached();
+    const int sms = device_sm_count();
     GRNND_CUDA(cudaMemsetAsync(w.in_count, 0, sizeof(int32_t) * (size_t)(n + 1), st));
     GRNND_CUDA(cudaMemsetAsync(w.ctr + C_HEAVY, 0, sizeof(unsigned long long), st));
     const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)sms * 8));
@@ -404,7 +391,7 @@ int launch_compact(const int32_t *msg_tgt, const int32_t *msg_id, const float *m
                    int64_t n, int32_t cap, const int64_t *offs, int32_t *flat_tgt, int32_t *flat_id,
                    float *flat_dist, int32_t *flat_src, cudaStream_t st) {
     if (n <= 0) return GRNND_OK;
-    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, (int64_t)num_sms_cached() * 16));
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, (int64_t)device_sm_count() * 16));
     compact_kernel<<<g, 256, 0, st>>>(msg_tgt, msg_id, msg_dist, msg_cnt, n, cap, offs, flat_tgt, flat_id,
                                       flat_dist, flat_src);
     return check_launch("compact_kernel");
@@ -484,7 +471,7 @@ __global__ void unpack_kernel(Workspace w, int64_t m, int64_t lo, int64_t n) {
 
 int launch_unpack(const Workspace &w, int64_t m, int64_t lo, int64_t n, cudaStream_t st) {
     if (m <= 0) return GRNND_OK;
-    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)num_sms_cached() * 8));
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)device_sm_count() * 8));
     unpack_kernel<<<g, 256, 0, st>>>(w, m, lo, n);
     return check_launch("unpack_kernel");
 }
@@ -499,7 +486,7 @@ int launch_bucket_by_rank(const Workspace &w, const int64_t *rank_bounds, int32_
     unsigned long long *rc = (unsigned long long *)w.scan_tmp;
     unsigned long long *cursor = rc + MAX_RANKS;
     GRNND_CUDA(cudaMemsetAsync(rc, 0, sizeof(unsigned long long) * MAX_RANKS, st));
-    const unsigned g = (unsigned)num_sms_cached() * 4;
+    const unsigned g = (unsigned)device_sm_count() * 4;
     rank_count_kernel<<<g, 256, 0, st>>>(w, rank_bounds, nranks, rc);
     rank_offsets_kernel<<<1, 32, 0, st>>>(rc, nranks, cursor, send_counts);
     rank_scatter_kernel<<<g, 256, 0, st>>>(w, rank_bounds, nranks, cursor);

@@ -57,38 +57,28 @@ __global__ void bin_kernel(const int32_t *__restrict__ read_count, int64_t n, in
                            const float *__restrict__ read_dists, int64_t lo, uint64_t seed, uint64_t stream_id,
                            int order_code, int32_t *__restrict__ msg_tgt, int32_t *__restrict__ msg_id,
                            float *__restrict__ msg_dist, int32_t *__restrict__ msg_cnt, int tc_bins) {
+    // thread = vertex for the binning; the Fisher-Yates hashes (the costly part, ~k x 100
+    // instructions per vertex) are computed warp-cooperatively for the warp's 32 vertices,
+    // so a warp costs sum(ceil(k / 32)) hash rounds instead of max(k); each lane then runs
+    // its own vertex's (cheap) swap chain from the staged swap targets.
     __shared__ unsigned long long s_sum;
-    extern __shared__ uint8_t fy_scratch[];  // [blockDim.x][cap]
+    extern __shared__ uint8_t fy_scratch[];  // [blockDim.x][cap] perm + [blockDim.x][cap] swap targets
     if (threadIdx.x == 0) s_sum = 0;
     __syncthreads();
+    const int lane = lane_id();
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int k = 0;
+    int k = 0, b = 0;
     if (v < n) {
         k = read_count[v];
-        const int b = bin_of(k, tc_bins);
+        b = bin_of(k, tc_bins);
         if (b > 0) {
             const unsigned peers = __match_any_sync(__activemask(), b);
             const int leader = __ffs(peers) - 1;
             unsigned long long base = 0;
-            if (lane_id() == leader) base = atomicAdd(&w.ctr[C_BIN0 + b], (unsigned long long)__popc(peers));
+            if (lane == leader) base = atomicAdd(&w.ctr[C_BIN0 + b], (unsigned long long)__popc(peers));
             base = __shfl_sync(peers, base, leader);
-            const int rank = __popc(peers & ((1u << lane_id()) - 1));
+            const int rank = __popc(peers & ((1u << lane) - 1));
             w.bins[(int64_t)b * w.n + (int64_t)base + rank] = make_int2((int)v, k);
-            if (order_code == 0) {
-                // perm = identity; for i = k-1..1: swap(perm[i], perm[hash4(seed,stream,v,i) % (i+1)])
-                // (per-thread scratch in shared memory, not local memory)
-                uint8_t *perm = fy_scratch + threadIdx.x * cap;
-                for (int i = 0; i < k; ++i) perm[i] = (uint8_t)i;
-                const uint64_t pre = vertex_prefix(seed, stream_id, (uint64_t)(lo + v));
-                for (int i = k - 1; i > 0; --i) {
-                    const int j = (int)mod_small(mix64(pre ^ (uint64_t)i), (uint32_t)(i + 1));
-                    const uint8_t t = perm[i];
-                    perm[i] = perm[j];
-                    perm[j] = t;
-                }
-                uint8_t *pos = w.pos8 + v * w.pcap;
-                for (int x = 0; x < k; ++x) pos[perm[x]] = (uint8_t)x;
-            }
         } else if (slice_mode) {
             // k <= 1: no pairs; the lone live entry (if any) survives (:186-192)
             int c = 0;
@@ -101,9 +91,39 @@ __global__ void bin_kernel(const int32_t *__restrict__ read_count, int64_t n, in
             msg_cnt[v] = c;
         }
     }
+    if (order_code == 0) {
+        // perm = identity; for i = k-1..1: swap(perm[i], perm[hash4(seed,stream,v,i) % (i+1)])
+        uint8_t *perm = fy_scratch + threadIdx.x * cap;
+        uint8_t *warp_j = fy_scratch + (size_t)blockDim.x * cap + (threadIdx.x - lane) * cap;
+        const int kk = b > 0 ? k : 0;
+        const uint64_t pre = vertex_prefix(seed, stream_id, (uint64_t)(lo + v));
+        unsigned todo = __ballot_sync(FULL, kk > 1);
+        while (todo) {
+            const int u = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int ku = __shfl_sync(FULL, kk, u);
+            const uint64_t pu = ((uint64_t)__shfl_sync(FULL, (unsigned)(pre >> 32), u) << 32) |
+                                (uint64_t)__shfl_sync(FULL, (unsigned)pre, u);
+            uint8_t *ju = warp_j + u * cap;
+            for (int i = lane + 1; i < ku; i += 32) ju[i] = (uint8_t)mod_small(mix64(pu ^ (uint64_t)i), (uint32_t)(i + 1));
+        }
+        __syncwarp();
+        if (kk > 1) {
+            const uint8_t *jv = warp_j + lane * cap;
+            for (int i = 0; i < kk; ++i) perm[i] = (uint8_t)i;
+            for (int i = kk - 1; i > 0; --i) {
+                const int j = jv[i];
+                const uint8_t t = perm[i];
+                perm[i] = perm[j];
+                perm[j] = t;
+            }
+            uint8_t *pos = w.pos8 + v * w.pcap;
+            for (int x = 0; x < kk; ++x) pos[perm[x]] = (uint8_t)x;
+        }
+    }
     unsigned long long ks = (unsigned long long)k;
     ks = warp_sum(ks);
-    if (lane_id() == 0 && ks) atomicAdd(&s_sum, ks);
+    if (lane == 0 && ks) atomicAdd(&s_sum, ks);
     __syncthreads();
     if (threadIdx.x == 0 && s_sum && stats) atomicAdd((unsigned long long *)&stats[GRNND_ST_MESSAGES], s_sum);
 }
@@ -429,11 +449,19 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) decide_kernel(PropArgs a) {
     const int cap = a.cap;
     int32_t *ids = sm.ids[wib];
     uint8_t *pos = sm.pos[wib];
-    unsigned long long red_total = 0, refp_total = 0;
+    unsigned long long red_total = 0, refp_total = 0, recpools = 0;
 
     for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
         const int k = a.read_count[v];
         if (k < 2) continue;  // no pairs (slice-mode survivors of k <= 1 come from bin_kernel)
+        const int ncl_all = a.w.clcnt[v];
+        if (!a.slice_mode && ncl_all == 0) {
+            // no redirect-capable pair: nothing is emitted or tombstoned (survivors stay in the
+            // row, which the round API keeps packed), and the reference visits every pair
+            if (lane == 0) refp_total += (unsigned long long)k * (unsigned long long)(k - 1) / 2ull;
+            continue;
+        }
+        recpools += ncl_all > 0 ? 1ull : 0ull;
         for (int s = lane; s < k; s += 32) {
             ids[s] = a.read_ids[v * cap + s];
             pos[s] = a.w.pos8[v * a.w.pcap + s];
@@ -443,7 +471,6 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) decide_kernel(PropArgs a) {
         // redirect-capable pairs (workspace.cuh PAIR_LIST): a complete list replaces the masks
         const int lcap = list_cap(cap);
         const int32_t *rec = a.w.clrec + v * (int64_t)CLREC;
-        const int ncl_all = a.w.clcnt[v];
         const bool from_list = ncl_all <= lcap;
         const int ncl = ncl_all < lcap ? ncl_all : lcap;
         int2 e0 = make_int2(0, 0), e1 = make_int2(0, 0);
@@ -496,22 +523,13 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) decide_kernel(PropArgs a) {
     if (lane == 0 && a.stats) {
         if (red_total) atomicAdd((unsigned long long *)&a.stats[GRNND_ST_REDIRECTS], red_total);
         if (refp_total) atomicAdd((unsigned long long *)&a.stats[GRNND_ST_PAIRS_REF], refp_total);
+        if (recpools) atomicAdd((unsigned long long *)&a.stats[GRNND_ST_RECPOOLS], recpools);
     }
 }
 
 #include "tc_pairs.cuh"
 #include "tc3_pairs.cuh"
 
-static int sm_count() {
-    static int s = 0;
-    if (!s) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
-        if (s <= 0) s = 148;
-    }
-    return s;
-}
 
 // ---------------------------------------------------------------------------------
 // squared row norms for the filtered pair phase (warp per row, any summation order:
@@ -546,7 +564,7 @@ void filter_eps(int32_t dim, float *eps_n, float *eps_h) {
 
 int launch_row_norms(const float *data, int64_t n, int32_t dim, int32_t ld, float *out, cudaStream_t st) {
     if (n <= 0) return GRNND_OK;
-    const int64_t blocks = std::min<int64_t>((n + 7) / 8, (int64_t)sm_count() * 32);
+    const int64_t blocks = std::min<int64_t>((n + 7) / 8, (int64_t)device_sm_count() * 32);
     row_norms_kernel<<<(unsigned)blocks, 256, 0, st>>>(data, n, dim, ld, out);
     return check_launch("row_norms_kernel");
 }
@@ -560,18 +578,15 @@ static int launch_pairs_impl(const PropArgs &a, int bin, cudaStream_t st) {
     const int nq_total = (a.dim + 3) >> 2;
     const int rs4 = row_stride16(nq_total);
     const size_t smem = align_up(sizeof(PairSmem<MAXK, B>), 128) + (size_t)B * kmax * rs4 * 16;
-    static int configured_smem = 0;
-    if ((int)smem > configured_smem) {
-        GRNND_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured_smem = (int)smem;
-    }
+    static SmemOptIn optin;
+    GRNND_CUDA(optin.ensure(kern, smem));
     int per_sm = 0;
     GRNND_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem));
     if (per_sm < 1) {
         set_error("pairs bin %d: no CTA fits (smem %zu B)", bin, smem);
         return GRNND_EUNSUPPORTED;
     }
-    kern<<<sm_count() * per_sm, THREADS, smem, st>>>(a, bin, kmax);
+    kern<<<device_sm_count() * per_sm, THREADS, smem, st>>>(a, bin, kmax);
     return check_launch("pairs_kernel");
 }
 
@@ -595,12 +610,9 @@ template <int SZ>
 static int launch_tc_pairs(const PropArgs &a, int bin, cudaStream_t st) {
     auto kern = tc_pairs_kernel<SZ>;
     const size_t smem = (size_t)TC_NSTAGE * TC_STAGE_BYTES + sizeof(TcSmem<SZ>) + 1024;
-    static bool configured = false;
-    if (!configured) {
-        GRNND_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = true;
-    }
-    kern<<<sm_count(), TC_THREADS, smem, st>>>(a, bin);
+    static SmemOptIn optin;
+    GRNND_CUDA(optin.ensure(kern, smem));
+    kern<<<device_sm_count(), TC_THREADS, smem, st>>>(a, bin);
     return check_launch("tc_pairs_kernel");
 }
 
@@ -608,12 +620,9 @@ template <int SZ>
 static int launch_tc3_pairs(const PropArgs &a, int bin, cudaStream_t st) {
     auto kern = tc3_pairs_kernel<SZ>;
     const size_t smem = (size_t)T3_NS * T3_STAGE + T3_PAD + sizeof(T3Smem<SZ>) + 1024;
-    static bool configured = false;
-    if (!configured) {
-        GRNND_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = true;
-    }
-    kern<<<sm_count(), T3_NT, smem, st>>>(a, bin);
+    static SmemOptIn optin;
+    GRNND_CUDA(optin.ensure(kern, smem));
+    kern<<<device_sm_count(), T3_NT, smem, st>>>(a, bin);
     return check_launch("tc3_pairs_kernel");
 }
 
@@ -629,7 +638,11 @@ int launch_propagate(const PropArgs &a, cudaStream_t st) {
     GRNND_CUDA(cudaMemsetAsync(a.w.clcnt, 0, sizeof(int32_t) * (size_t)n, st));
     const bool tc3 = GRNND_TC && a.norms && a.dim <= 128 && a.cap <= T3_ROWS && a.order_code == 0;
     const int tb = 128;
-    bin_kernel<<<(unsigned)((n + tb - 1) / tb), tb, (size_t)tb * a.cap, st>>>(a.read_count, n, a.cap, a.w, a.stats, a.slice_mode,
+    {
+        static SmemOptIn optin;
+        GRNND_CUDA(optin.ensure(bin_kernel, (size_t)tb * a.cap * 2));
+    }
+    bin_kernel<<<(unsigned)((n + tb - 1) / tb), tb, (size_t)tb * a.cap * 2, st>>>(a.read_count, n, a.cap, a.w, a.stats, a.slice_mode,
                                                             a.read_ids, a.read_dists, a.lo, a.seed, a.stream_id,
                                                             a.order_code, a.msg_tgt, a.msg_id, a.msg_dist,
                                                             a.msg_cnt, tc3 ? 1 : 0);
@@ -637,7 +650,7 @@ int launch_propagate(const PropArgs &a, cudaStream_t st) {
     // largest k first so long CTAs start early
     if (a.cap > 128) GRNND_TRY((launch_pairs<256, 1, 256, 3, 4>(a, 5, st)));
     if (tc3) {
-        tc_stage_kernel<<<sm_count() * 8, 256, 0, st>>>(a);
+        tc_stage_kernel<<<device_sm_count() * 8, 256, 0, st>>>(a);
         GRNND_TRY(check_launch("tc_stage_kernel"));
         if (a.cap > 48) GRNND_TRY(launch_tc3_pairs<96>(a, 6, st));
         if (a.cap > 32) GRNND_TRY(launch_tc3_pairs<48>(a, 5, st));
@@ -659,7 +672,7 @@ int launch_propagate(const PropArgs &a, cudaStream_t st) {
     if (a.cap > 16) GRNND_TRY((launch_pairs<32, GRNND_B2_BATCH, 128, 3, 2>(a, 2, st)));
     if (a.cap > 1) GRNND_TRY((launch_pairs<16, GRNND_B1_BATCH, 128, 2, 2>(a, 1, st)));
     }
-    const int64_t blocks = std::min<int64_t>((n + DEC_WARPS - 1) / DEC_WARPS, (int64_t)sm_count() * 16);
+    const int64_t blocks = std::min<int64_t>((n + DEC_WARPS - 1) / DEC_WARPS, (int64_t)device_sm_count() * 16);
     const unsigned g = (unsigned)std::max<int64_t>(1, blocks);
     switch (a.w.mw) {
         case 1: decide_kernel<1><<<g, DEC_WARPS * 32, 0, st>>>(a); break;
@@ -675,11 +688,11 @@ int launch_propagate(const PropArgs &a, cudaStream_t st) {
 
 #ifdef GRNND_T3_PROF
 // profiling builds only: role timers of tc3_pairs_kernel (read and reset)
-extern "C" int grnnd_debug_counters(unsigned long long *out, int n) {
-    unsigned long long buf[32] = {0};
+extern "C" int grnnd_debug_counters(unsigned long long *out, int n) {  // [8 bins][32]
+    unsigned long long buf[256] = {0};
     if (cudaMemcpyFromSymbol(buf, grnnd::g_t3prof, sizeof(buf)) != cudaSuccess) return GRNND_ECUDA;
-    for (int i = 0; i < n && i < 32; ++i) out[i] = buf[i];
-    unsigned long long z[32] = {0};
+    for (int i = 0; i < n && i < 256; ++i) out[i] = buf[i];
+    unsigned long long z[256] = {0};
     if (cudaMemcpyToSymbol(grnnd::g_t3prof, z, sizeof(z)) != cudaSuccess) return GRNND_ECUDA;
     return GRNND_OK;
 }

@@ -123,19 +123,9 @@ __global__ void merge_slices_kernel(ReverseArgs a) {
     }
 }
 
-static int sms() {
-    static int s = 0;
-    if (!s) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
-        if (s <= 0) s = 148;
-    }
-    return s;
-}
 
 static unsigned warp_grid(int64_t n) {
-    const int64_t blocks = std::min<int64_t>((n + 7) / 8, (int64_t)sms() * 16);
+    const int64_t blocks = std::min<int64_t>((n + 7) / 8, (int64_t)device_sm_count() * 16);
     return (unsigned)std::max<int64_t>(1, blocks);
 }
 

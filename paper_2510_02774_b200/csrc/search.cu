@@ -260,7 +260,7 @@ constexpr int GS_LMAX = 1024;
 
 __host__ __device__ inline size_t gs_warp_bytes(int ld, int L) {
     // query row, 2 x (ids, dists, expanded) list halves, 32 new keys
-    return align_up((size_t)ld * 4, 16) + 2 * ((size_t)L * 9 + 16) + 32 * 8 + 64;
+    return align_up(align_up((size_t)ld * 4, 16) + 2 * align_up((size_t)L * 9, 16) + 32 * 8 + 64, 16);
 }
 
 // keys < (d, i) in the sorted (dist, id) array [0, n)
@@ -288,11 +288,11 @@ __global__ void __launch_bounds__(GS_WARPS * 32) greedy_kernel(const int64_t *__
     unsigned char *my = gs_raw + (size_t)w * gs_warp_bytes(ld, L);
     float *qrow = reinterpret_cast<float *>(my);
     unsigned char *lb = my + align_up((size_t)ld * 4, 16);
-    const size_t hb = (size_t)L * 9 + 16;  // bytes of one list half: ids, dists, expanded flags
+    const size_t hb = align_up((size_t)L * 9, 16);  // bytes of one list half: ids, dists, expanded flags
     auto hid = [&](int hh) { return reinterpret_cast<int *>(lb + hh * hb); };
     auto hds = [&](int hh) { return reinterpret_cast<float *>(lb + hh * hb + (size_t)L * 4); };
     auto hex = [&](int hh) { return lb + hh * hb + (size_t)L * 8; };
-    float *nd = reinterpret_cast<float *>(lb + 2 * ((size_t)L * 9 + 16));
+    float *nd = reinterpret_cast<float *>(lb + 2 * hb);
     int *ni = reinterpret_cast<int *>(nd + 32);
     const int nq4 = ld >> 2;
     for (int c = lane; c < nq4; c += 32)
@@ -420,16 +420,10 @@ __global__ void normalize_rows_kernel(float *__restrict__ data, int64_t n, int32
     for (int d = 0; d < dim; ++d) row[d] = __fdiv_rn(row[d], nr);
 }
 
-static int device_sms() {
-    int dev = 0, s = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
-    return s > 0 ? s : 148;
-}
 
 int64_t bf_chunks(int64_t n, int64_t nq) {
     const int64_t qblocks = (nq + BF_QB - 1) / BF_QB;
-    int64_t want = ((int64_t)device_sms() * 4 + qblocks - 1) / qblocks;
+    int64_t want = ((int64_t)device_sm_count() * 4 + qblocks - 1) / qblocks;
     const int64_t maxc = (n + BF_TILE - 1) / BF_TILE;
     if (want > maxc) want = maxc;
     if (want > 65535) want = 65535;
@@ -479,7 +473,8 @@ int grnnd_brute_force(const float *data, int64_t n, int32_t dim, int32_t ld, con
     int32_t *pi = reinterpret_cast<int32_t *>(pd + (size_t)nq * nc * k);
     const int64_t chunk = ((n + nc - 1) / nc + BF_TILE - 1) / BF_TILE * BF_TILE;
     const int64_t nc_eff = (n + chunk - 1) / chunk;
-    GRNND_CUDA(cudaFuncSetAttribute(bf_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)z.total));
+    static SmemOptIn optin;
+    GRNND_CUDA(optin.ensure(bf_partial_kernel, z.total));
     dim3 grid((unsigned)((nq + BF_QB - 1) / BF_QB), (unsigned)nc_eff);
     bf_partial_kernel<<<grid, BF_TILE, z.total, st>>>(data, n, ld, queries, nq, k, chunk, pd, pi);
     GRNND_TRY(check_launch("bf_partial_kernel"));
@@ -518,7 +513,8 @@ int grnnd_greedy_search(const int64_t *offsets, const int32_t *nbrs, int64_t n, 
         return GRNND_EUNSUPPORTED;
     }
     GRNND_CUDA(cudaMemsetAsync(visited, 0, need, st));
-    GRNND_CUDA(cudaFuncSetAttribute(greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    static SmemOptIn optin;
+    GRNND_CUDA(optin.ensure(greedy_kernel, smem));
     greedy_kernel<<<(unsigned)((nq + GS_WARPS - 1) / GS_WARPS), GS_WARPS * 32, smem, st>>>(
         offsets, nbrs, data, ld, queries, nq, L, k, entries, reinterpret_cast<uint32_t *>(visited), (n + 31) / 32,
         out_ids, out_dists, out_cnt);

@@ -122,7 +122,7 @@ __device__ __forceinline__ int64_t tc_group_base(const unsigned long long *ctr, 
 }
 
 #ifdef GRNND_T3_PROF
-__device__ unsigned long long g_t3prof[32];
+__device__ unsigned long long g_t3prof[8][32];  // per TC bin
 __device__ long long g_t3trace[64][10];  // CTA 0: per group event times (profiling builds)
 #define T3P_BEGIN() const long long _t3p0 = clock64()
 #define T3P_EV(g, ev) do { if (blockIdx.x == 0 && (g) < 64) g_t3trace[(g)][(ev)] = clock64(); } while (0)
@@ -368,6 +368,41 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                     cm |= !(lhs >= rhs) ? (1u << c) : 0u;
                 }
                 cm &= vm;
+#ifdef GRNND_TC_VALIDATE
+                // validation builds: every screened pair's |d~ - d_exact| against the bound
+                // TC_EPS (|a|^2 + |b|^2) the filter relies on (the stage is still resident)
+                if (a.stats) {
+                    const unsigned char *stg = base + (int)(g % NS) * T3_STAGE;
+                    uint32_t vv = vm;
+                    unsigned long long chk = 0, bad = 0;
+                    float worst = 0.0f;
+                    while (vv) {
+                        const int c = __ffs(vv) - 1;
+                        vv &= vv - 1u;
+                        const int jr = cb + c, ii = tr ? jr : i, jj = tr ? i : jr;
+                        float dx = 0.0f;
+                        for (int q = 0; q < nq; ++q) {
+                            const float4 x = *reinterpret_cast<const float4 *>(stg + t3_off(ii, q));
+                            const float4 y = *reinterpret_cast<const float4 *>(stg + t3_off(jj, q));
+                            dx = exact_step(dx, x.x, y.x);
+                            dx = exact_step(dx, x.y, y.y);
+                            dx = exact_step(dx, x.z, y.z);
+                            dx = exact_step(dx, x.w, y.w);
+                        }
+                        const float nn = mt.nrm[i] + mt.nrm[jr];
+                        const float err = fabsf(fmaf(-2.0f, __uint_as_float(r[c]), nn) - dx);
+                        const float ratio = err / fmaf(TC_EPS, nn, 1e-30f);
+                        worst = ratio > worst ? ratio : worst;
+                        bad += ratio > 1.0f ? 1ull : 0ull;
+                        ++chk;
+                    }
+                    if (chk) {
+                        atomicMax((int *)&a.stats[GRNND_ST_TCV_MAX_RATIO], __float_as_int(worst));
+                        atomicAdd((unsigned long long *)&a.stats[GRNND_ST_TCV_CHECKED], chk);
+                        if (bad) atomicAdd((unsigned long long *)&a.stats[GRNND_ST_TCV_VIOLATIONS], bad);
+                    }
+                }
+#endif
                 if (__any_sync(FULL, cm != 0u)) {
                     const int n = __popc(cm);
                     int qi = n ? atomicAdd(&sm.qn[b], n) : 0;
@@ -658,7 +693,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
     tc::fence_before();
     __syncthreads();
 #ifdef GRNND_T3_PROF
-    if (tid < 32 && t3p_sm[tid]) atomicAdd(&g_t3prof[tid], t3p_sm[tid]);
+    if (tid < 32 && t3p_sm[tid]) atomicAdd(&g_t3prof[bin][tid], t3p_sm[tid]);
 #endif
     if (warp == 1) tc::tmem_dealloc(tmem, TC_TMEM_COLS);
     if (a.stats) {

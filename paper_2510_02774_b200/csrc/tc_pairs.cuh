@@ -332,9 +332,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_pairs_kernel(PropArgs a, int
                     const float dx = exact_rows(stg, i, jr);
                     const float err = fabsf(fmaf(-2.0f, __uint_as_float(r[c]), nn) - dx);
                     const float ratio = err / fmaf(TC_EPS, nn, 1e-30f);
-                    atomicMax((int *)&a.stats[14], __float_as_int(ratio));  // ratio >= 0: int order = float order
-                    if (ratio > 1.0f) atomicAdd((unsigned long long *)&a.stats[15], 1ull);
-                    atomicAdd((unsigned long long *)&a.stats[13], 1ull);
+                    atomicMax((int *)&a.stats[GRNND_ST_TCV_MAX_RATIO], __float_as_int(ratio));  // ratio >= 0: int order = float order
+                    if (ratio > 1.0f) atomicAdd((unsigned long long *)&a.stats[GRNND_ST_TCV_VIOLATIONS], 1ull);
+                    atomicAdd((unsigned long long *)&a.stats[GRNND_ST_TCV_CHECKED], 1ull);
                 }
 #endif
             }

@@ -178,6 +178,9 @@ def test_whole_builds_bit_exact_vs_reference(g, golden):
         (3000, 24, "clustered", 16, 130, 2, 3, 9),   # R > 128: propagate bin 5, apply RPL 5
         (4000, 200, "gaussian", 12, 40, 2, 2, 3),    # two 128-dim chunks
         (2000, 1, "uniform", 4, 8, 2, 3, 2),         # D = 1, many exact ties
+        (20000, 128, "gaussian", 20, 128, 4, 15, 1), # R = 128: the 96 < R <= 128 tensor-core path, full schedule
+        (12000, 128, "gaussian", 20, 100, 2, 8, 6),  # R = 100
+        (8000, 96, "clustered", 20, 112, 2, 6, 7),   # R = 112, D = 96
     ],
 )
 def test_build_bit_exact_vs_oracle(g, n, dim, dist, S, R, T1, T2, seed):
@@ -355,3 +358,30 @@ def test_filtered_phase_from_the_first_round(g, monkeypatch):
         graph = g.build(ds, g.BuildParams(S=20 if R > 20 else 16, R=R, T1=2, T2=4, rho=0.6, seed=seed))
         off, nb = oracle.build(ds.data, 20 if R > 20 else 16, R, 2, 4, 0.6, seed)
         assert np.array_equal(graph.offsets, off) and np.array_equal(graph.neighbor_ids, nb), (n, dim, dist, R)
+
+
+# ------------------------------------------------------------------ direct fixture tests (reference outputs)
+def test_init_dists_and_merge_messages_bit_exact(K, golden):
+    """kernels.init_dists (_numba_kernels.py:118-122) and gen_merge_messages (:236-250) on
+    the reference's own stage fixtures."""
+    s = golden("stages")
+    for name in ("gauss16", "int8", "clust4", "gauss128"):
+        data, rid, rd, rc = s[f"{name}_data"], s[f"{name}_rid"], s[f"{name}_rd"], s[f"{name}_rc"]
+        n, cap = rid.shape
+        live = np.arange(cap)[None, :] < rc[:, None]
+        ids = np.where(live, rid, (np.arange(n, dtype=np.int32)[:, None] + 1) % n).astype(np.int32)
+        out = np.zeros((n, cap), np.float32)
+        K.init_dists(data, ids, out)
+        # the reference's pools store its own _sqdist of (v, id): equal bits on the live prefix
+        assert np.array_equal(out[live].view(np.uint32), rd[live].view(np.uint32)), name
+        assert np.array_equal(out.view(np.uint32), oracle.init_dists(data, ids).view(np.uint32))
+        mt = np.full(n * cap, -7, np.int32)
+        mi = np.full(n * cap, -7, np.int32)
+        md = np.full(n * cap, -7.0, np.float32)
+        mc = np.zeros(n, np.int32)
+        K.gen_merge_messages(rid, rd, rc, mt, mi, md, mc)
+        wt, wi, wd, wc = oracle.gen_merge_messages(rid, rd, rc)
+        assert np.array_equal(mc, wc), name
+        m = (np.arange(cap)[None, :] < mc[:, None]).ravel()
+        assert np.array_equal(mt[m], wt[m]) and np.array_equal(mi[m], wi[m]) and np.array_equal(md[m], wd[m])
+        assert np.all(mt[~m] == -7)  # untouched tails

@@ -12,7 +12,7 @@ ds = g.generate(1_000_000, 128, "gaussian", seed=1)
 p = g.BuildParams(S=20, R=96, T1=2, T2=15, rho=0.6, seed=1)
 st = g.init_neighbors(ds, p)
 row = torch.zeros(16, dtype=torch.int64, device="cuda")
-buf = (C.c_ulonglong * 32)()
+buf = (C.c_ulonglong * 256)()
 # slot, name, number of timed warps (lane 0 of each)
 rows = [(0, "meta wait mempty", 1), (1, "meta total", 1), (2, "mma wait full", 1), (3, "mma wait acce", 1),
         (17, "mma total", 1), (20, "mma fence", 1), (21, "mma commit", 1), (4, "filt wait mfull", 3), (5, "filt bar1", 3), (6, "filt wait qemp", 3),
@@ -21,12 +21,17 @@ rows = [(0, "meta wait mempty", 1), (1, "meta total", 1), (2, "mma wait full", 1
 for r in range(25):
     st.pools.update(p.seed, 1 + st.round_index, 0, row); st.round_index += 1
     torch.cuda.synchronize()
-    lib.grnnd_debug_counters(buf, 32)
+    lib.grnnd_debug_counters(buf, 256)
     if r in (0, 24):
-        v = list(buf)
-        print(f"round {r + 1}: groups {v[12]}")
-        for slot, name, w in rows:
-            print(f"   {name:22s} {v[slot] / max(v[12], 1) / w:10.0f} cycles/group")
+        allv = list(buf)
+        for b in range(1, 7):
+            v = allv[32 * b: 32 * b + 32]
+            if not v[12]:
+                continue
+            print(f"round {r + 1} bin {b} (slot {96 // (12, 6, 4, 3, 2, 1)[b - 1]}): groups {v[12]}, "
+                  f"CTA-cycles/group {v[1] / max(v[12], 1):.0f}")
+            for slot, name, w in rows:
+                print(f"   {name:22s} {v[slot] / max(v[12], 1) / w:10.0f} cycles/group")
 tr = (C.c_longlong * 640)()
 lib.grnnd_debug_trace(tr)
 t = np.array(list(tr)).reshape(64, 10)

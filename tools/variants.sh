@@ -6,7 +6,7 @@ cd "$(dirname "$0")/../paper_2510_02774_b200/csrc"
 while [ $# -ge 2 ]; do
   name=$1; flags=$2; shift 2
   out=../_build/variants/$name; mkdir -p $out/obj
-  for f in capi propagate group apply reverse; do
+  for f in capi propagate group apply reverse search; do
     /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
       -Xcompiler -fPIC,-O2 -I../../include -I. --expt-relaxed-constexpr $flags -c $f.cu -o $out/obj/$f.o &
   done
