@@ -315,6 +315,14 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     apply_ms = [b.elapsed_time(c) for _, b, c in phase]
     edges = int(offsets[-1].item())
 
+    # ---- parity (outside the timed regions), then free the engine for the e2e leg ----
+    parity = None
+    if rank == 0 and world == 1 and not args.no_parity:
+        parity = parity_leg(args, g, eng.search_data(), offsets, nbrs, edges)
+    del out, offsets, nbrs, bad, fail, eng
+    data_dev = None
+    torch.cuda.empty_cache()
+
     # ---- e2e through the public API, host buffers (pinned) ----
     host = torch.from_numpy(data).pin_memory()
     pinned_ds = g.Dataset(host.numpy())
@@ -355,10 +363,6 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
         traffic = json.loads(NCU_FILE.read_text()).get("dram_bytes_per_round")
     except Exception:
         pass
-
-    parity = None
-    if rank == 0 and world == 1 and not args.no_parity:
-        parity = parity_leg(args, g, eng.search_data(), offsets, nbrs, edges)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -482,7 +482,7 @@ class BuildState:
 
 
 def init_neighbors(dataset: Dataset, params: BuildParams, pair_order: PairOrder = "disordered",
-                   *, device=None, metric: str = "l2") -> BuildState:
+                   *, device=None, metric: str = "l2", msg_capacity: int | None = None) -> BuildState:
     """S distinct random neighbours != owner per vertex (builder.py:221-257).  The
     reference validates the dataset (finiteness included) before the parameters; so does
     this, with the finiteness scan on the device."""
@@ -500,7 +500,7 @@ def init_neighbors(dataset: Dataset, params: BuildParams, pair_order: PairOrder 
             raise ParamError("S <= N-1")
         if metric == "ip":
             normalize_rows_(data_dev, dataset.dim)
-    pools = _DevicePools(data_dev, dataset.dim, params.R)
+    pools = _DevicePools(data_dev, dataset.dim, params.R, msg_capacity=msg_capacity)
     fail = pools.init(params.S, params.seed)
     if int(fail.item()):  # pragma: no cover - probability ~ exp(-64)
         raise RuntimeError("initial neighbor sampling did not converge")
@@ -590,18 +590,40 @@ def run_rounds(state: BuildState, stats_rows: torch.Tensor | None = None) -> lis
     return kinds
 
 
+MSG_PER_ROW = 48  # optimistic message capacity per owned row (see build())
+
+
+def optimistic_msg_capacity(rows: int, cap: int) -> int:
+    """Message slots a build starts with: MSG_PER_ROW per row instead of the worst case
+    rows * R (an update round emits one redirect per tombstoned entry, <= sum(k); a reverse
+    round ceil(rho k) per row).  At C2 the largest round needs ~20 per row; the worst case
+    would cost 60 B x R per row of workspace (5.8 GB at 1M x 96)."""
+    return int(min(max(rows * cap, 1), max(MSG_PER_ROW * rows, 1 << 16)))
+
+
 def build(dataset: Dataset, params: BuildParams, pair_order: PairOrder = "disordered",
           report_stats: list | None = None, *, device=None, metric: str = "l2") -> Graph:
     """Full build (builder.py:365-390): init, T1 x T2 pair rounds with reverse-edge
     sampling between outer iterations, then graph emission.  One host sync for the
     init-failure flag, one at the end; every round is a single asynchronous call.
-    ``metric="ip"`` builds over L2-normalised rows (inner product; not in the reference)."""
+    ``metric="ip"`` builds over L2-normalised rows (inner product; not in the reference).
+
+    The workspace starts with an optimistic message capacity; a round that outgrows it
+    loses messages, which the device counts (GRNND_ST_LOST) -- the stats rows are read
+    before the graph is emitted and such a build is redone once at the worst-case
+    capacity, so a result is never built on dropped messages."""
     params = effective_params(params, dataset.num_points)
-    state = init_neighbors(dataset, params, pair_order, device=device, metric=metric)
-    rows = torch.zeros((num_rounds(params), _lib.NSTATS), dtype=torch.int64, device=state.pools.dev)
-    kinds = run_rounds(state, rows)
+    for attempt in range(2):
+        cap_msgs = optimistic_msg_capacity(dataset.num_points, params.R) if attempt == 0 else None
+        state = init_neighbors(dataset, params, pair_order, device=device, metric=metric, msg_capacity=cap_msgs)
+        rows = torch.zeros((num_rounds(params), _lib.NSTATS), dtype=torch.int64, device=state.pools.dev)
+        kinds = run_rounds(state, rows)
+        host_rows = rows.cpu().numpy()
+        if attempt == 0 and host_rows[:, _lib.ST_LOST].any():
+            del state, rows
+            continue
+        break
     graph = finalize_graph(state)
-    host_rows = rows.cpu().numpy()
     for kind, c in zip(kinds, host_rows):
         s = RoundStats.from_counters(kind, c)
         _accumulate(state.totals, s)
@@ -616,7 +638,7 @@ class DeviceBuild:
     finalize, entirely asynchronous; results stay in HBM."""
 
     def __init__(self, data_dev: torch.Tensor, dim: int, params: BuildParams,
-                 pair_order: PairOrder = "disordered", metric: str = "l2"):
+                 pair_order: PairOrder = "disordered", metric: str = "l2", msg_capacity: int | None = None):
         self.params = effective_params(params, int(data_dev.shape[0]))
         validate_params(self.params, int(data_dev.shape[0]))
         check_metric(metric)
@@ -626,7 +648,10 @@ class DeviceBuild:
         self.dim = dim
         # IP: every run normalises a copy of the raw vectors (part of the timed build)
         work = torch.empty_like(data_dev) if metric == "ip" else data_dev
-        self.pools = _DevicePools(work, dim, self.params.R)
+        # optimistic message capacity (build()); round_stats() raises if a round outgrew it
+        mc = msg_capacity if msg_capacity is not None else optimistic_msg_capacity(int(data_dev.shape[0]),
+                                                                                    self.params.R)
+        self.pools = _DevicePools(work, dim, self.params.R, msg_capacity=mc)
         self.rounds = num_rounds(self.params)
         self.stats = torch.zeros((self.rounds, _lib.NSTATS), dtype=torch.int64, device=self.pools.dev)
         self.kinds: list[str] = []

@@ -261,10 +261,13 @@ __device__ __forceinline__ uint64_t bits_below(int f, int w) {  // bits of word 
     return (1ull << b) - 1ull;
 }
 
-constexpr int DEC_WARPS = 8;
+// warps per decide CTA: 8 (R <= 128), 4 for the wider rows (static shared memory <= 48 KB)
+template <int MW>
+constexpr int dec_warps() { return MW <= 2 ? 8 : 4; }
 
 template <int MW>
 struct DecideSmem {
+    static constexpr int DEC_WARPS = dec_warps<MW>();
     static constexpr int CAPM = MW * 64;
     int32_t ids[DEC_WARPS][CAPM];
     int16_t perm[DEC_WARPS][CAPM];
@@ -272,13 +275,16 @@ struct DecideSmem {
     int16_t e_tgt[DEC_WARPS][CAPM];
     int16_t e_id[DEC_WARPS][CAPM];
     uint16_t e_key[DEC_WARPS][CAPM];  // (anchor pos << 8) | partner pos of message j
+    float e_d[DEC_WARPS][CAPM];       // kept exact distance of message j (NaN bits: not kept)
+    uint64_t bm[DEC_WARPS][32][MW];   // cond / afar words of the current 32-anchor block
+    uint64_t bf[DEC_WARPS][32][MW];
 };
 
 // The anchor-serial rule of one pool (SURVEY 7 hard part 1), warp-collective: anchors are
 // visited in permutation-position order; an anchor with a live redirect partner emits its
 // partner-far messages in position order up to the first anchor-far partner (which
 // redirects the anchor and ends its row).  masks(x, c, am) gives anchor x's cond / afar
-// words; dist_of(key, found) looks an emitted pair's exact distance up (warp-collective);
+// words; dist_of(key, j, nm, found) looks message j's exact distance up (warp-collective);
 // missing ones are re-evaluated from global rows.  Emits to the message list (or the
 // reference's slices), tombstones read_ids, counts redirects and reference-semantics pairs.
 template <int MW, class MaskFn, class DistFn>
@@ -388,7 +394,7 @@ __device__ __forceinline__ void decide_pool(const PropArgs &a, int k, int64_t v,
         const int j = jb + lane;
         const uint32_t mykey = j < nm ? (uint32_t)e_key[j] : 0xFFFFFFFFu;
         bool found = false;
-        float d = dist_of(mykey, found);
+        float d = dist_of(mykey, j, nm, found);
         if (j >= nm) continue;
         const int32_t tgt = ids[e_tgt[j]];
         const int32_t id = ids[e_id[j]];
@@ -441,7 +447,7 @@ __device__ __forceinline__ void decide_pool(const PropArgs &a, int k, int64_t v,
 }
 
 template <int MW>
-__global__ void __launch_bounds__(DEC_WARPS * 32) decide_kernel(PropArgs a) {
+__global__ void __launch_bounds__(dec_warps<MW>() * 32, 4) decide_kernel(PropArgs a) {
     __shared__ DecideSmem<MW> sm;
     const int lane = lane_id(), wib = threadIdx.x >> 5;
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -478,23 +484,33 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) decide_kernel(PropArgs a) {
         if (lane + 32 < ncl) e1 = *reinterpret_cast<const int2 *>(rec + 4 + 2 * (lane + 32));
         const uint32_t key0 = (uint32_t)e0.x, key1 = (uint32_t)e1.x;
         const float cd0 = __int_as_float(e0.y), cd1 = __int_as_float(e1.y);
+        uint64_t(*bm)[MW] = sm.bm[wib];
+        uint64_t(*bf)[MW] = sm.bf[wib];
+        // a complete list: each lane ORs its (<= 2) records of the current anchor block into
+        // the block's mask rows (instead of every lane scanning the whole list)
         auto masks = [&](int x, uint64_t (&c)[MW], uint64_t (&am)[MW]) {
             if (from_list) {
+                const int x0 = x - lane;
 #pragma unroll
-                for (int i = 0; i < MW; ++i) c[i] = am[i] = 0ull;
-                for (int t = 0; t < ncl; ++t) {
-                    const uint32_t kk = __shfl_sync(FULL, t < 32 ? key0 : key1, t & 31);
-                    if ((int)((kk >> 8) & 255u) == x) {
-                        const int xb = (int)(kk & 255u);
-                        const uint64_t bit = 1ull << (xb & 63);
+                for (int i = 0; i < MW; ++i) bm[lane][i] = bf[lane][i] = 0ull;
+                __syncwarp();
 #pragma unroll
-                        for (int i = 0; i < MW; ++i) {
-                            if (i == (xb >> 6)) {
-                                c[i] |= bit;
-                                if (kk >> 16) am[i] |= bit;
-                            }
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t kk = h ? key1 : key0;
+                    if (lane + 32 * h < ncl) {
+                        const int xr = (int)((kk >> 8) & 255u) - x0, xb = (int)(kk & 255u);
+                        if (xr >= 0 && xr < 32) {
+                            const uint64_t bit = 1ull << (xb & 63);
+                            atomicOr((unsigned long long *)&bm[xr][xb >> 6], bit);
+                            if (kk >> 16) atomicOr((unsigned long long *)&bf[xr][xb >> 6], bit);
                         }
                     }
+                }
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < MW; ++i) {
+                    c[i] = bm[lane][i];
+                    am[i] = bf[lane][i];
                 }
             } else {
 #pragma unroll
@@ -504,16 +520,24 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) decide_kernel(PropArgs a) {
                 }
             }
         };
-        auto dist_of = [&](uint32_t mykey, bool &found) -> float {
-            float d = 0.0f;
-            for (int t = 0; t < ncl; ++t) {
-                const uint32_t kk = __shfl_sync(FULL, t < 32 ? key0 : key1, t & 31) & 0xFFFFu;
-                const float dd = __shfl_sync(FULL, t < 32 ? cd0 : cd1, t & 31);
-                if (kk == mykey) {
-                    d = dd;
-                    found = true;
+        // kept distances scattered to their messages once (the records held by each lane
+        // against the nm emitted keys), then read by message index
+        float *e_d = sm.e_d[wib];
+        const uint16_t *ek = sm.e_key[wib];
+        auto dist_of = [&](uint32_t mykey, int j, int nm, bool &found) -> float {
+            if (j < 32) {  // first batch: scatter
+                for (int t = lane; t < nm; t += 32) e_d[t] = __int_as_float(0x7FFFFFFF);
+                __syncwarp();
+                for (int t = 0; t < nm; ++t) {
+                    const uint32_t et = ek[t];
+                    if (lane < ncl && (key0 & 0xFFFFu) == et) e_d[t] = cd0;
+                    if (lane + 32 < ncl && (key1 & 0xFFFFu) == et) e_d[t] = cd1;
                 }
+                __syncwarp();
             }
+            if (j >= nm) return 0.0f;
+            const float d = e_d[j];
+            found = __float_as_int(d) != 0x7FFFFFFF;
             return d;
         };
         decide_pool<MW>(a, k, v, ids, pos, sm.perm[wib], sm.e_tgt[wib], sm.e_id[wib], sm.e_key[wib], masks, dist_of,
@@ -672,13 +696,15 @@ int launch_propagate(const PropArgs &a, cudaStream_t st) {
     if (a.cap > 16) GRNND_TRY((launch_pairs<32, GRNND_B2_BATCH, 128, 3, 2>(a, 2, st)));
     if (a.cap > 1) GRNND_TRY((launch_pairs<16, GRNND_B1_BATCH, 128, 2, 2>(a, 1, st)));
     }
-    const int64_t blocks = std::min<int64_t>((n + DEC_WARPS - 1) / DEC_WARPS, (int64_t)device_sm_count() * 16);
-    const unsigned g = (unsigned)std::max<int64_t>(1, blocks);
+    auto dec = [&](auto kern, int warps) {
+        const int64_t blocks = std::min<int64_t>((n + warps - 1) / warps, (int64_t)device_sm_count() * 16);
+        kern<<<(unsigned)std::max<int64_t>(1, blocks), warps * 32, 0, st>>>(a);
+    };
     switch (a.w.mw) {
-        case 1: decide_kernel<1><<<g, DEC_WARPS * 32, 0, st>>>(a); break;
-        case 2: decide_kernel<2><<<g, DEC_WARPS * 32, 0, st>>>(a); break;
-        case 3: decide_kernel<3><<<g, DEC_WARPS * 32, 0, st>>>(a); break;
-        case 4: decide_kernel<4><<<g, DEC_WARPS * 32, 0, st>>>(a); break;
+        case 1: dec(decide_kernel<1>, dec_warps<1>()); break;
+        case 2: dec(decide_kernel<2>, dec_warps<2>()); break;
+        case 3: dec(decide_kernel<3>, dec_warps<3>()); break;
+        case 4: dec(decide_kernel<4>, dec_warps<4>()); break;
         default: set_error("cap %d > %d unsupported", a.cap, GRNND_MAX_CAP); return GRNND_EUNSUPPORTED;
     }
     return check_launch("decide_kernel");

@@ -500,12 +500,9 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             const int s = (int)(g % NS), m = (int)(g % NM), b = (int)(g & 1);
             const unsigned char *stg = base + s * T3_STAGE;
             const T3Meta &mt = sm.meta[m];
-            if (g >= 2) {  // group g - 2: record bulk stores have read the records, masks cleared
-                if (et == 0) {
-                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-#pragma unroll
-                    for (int p = 0; p < GP; ++p) sm.cl_n[b][p] = 0;
-                }
+            if (g >= 2) {  // group g - 2: record bulk stores have read the records (counts and
+                           // mask rows were cleared at the end of its epilogue)
+                if (et == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 tc::named_bar(bar_id, 96);
             }
             T3P_WAIT(9, tc::mbar_wait(&sm.qrdy[b], (uint32_t)((g >> 1) & 1)));
@@ -628,6 +625,9 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
 #ifdef GRNND_T3_PROF
             if (lane == 0) T3P_ADD(18, _tx0);
 #endif
+            // every thread that wrote pair records makes them visible to the async proxy (the
+            // bulk stores below read them) before the set's barrier
+            tc::fence_proxy_async();
             T3P_WAIT(10, tc::named_bar(bar_id, 96));  // masks + kept distances of group g complete
             if (et == 0) T3P_EV(g, 8);
 #ifdef GRNND_T3_PROF
@@ -641,6 +641,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             if (et < GP && mt.hdr[et].x >= 0) {
                 const int c = sm.cl_n[b][et];
                 sm.rec[b][et][0] = c;
+                tc::fence_proxy_async();  // the header, for the bulk store issued by et == 0
                 if (c > 0) {  // the counts were zeroed for the round
                     a.w.clcnt[mt.hdr[et].x] = c;
                     st_red += (unsigned long long)c;
@@ -682,6 +683,13 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             if (lane == 0) T3P_ADD(19, _tx1);
 #endif
             if (et == 0) T3P_EV(g, 9);
+            // every thread of the set is past its reads of the pair counts (the mask-row loop
+            // and the bulk-store sizes above): only now may they be reset for group g + 2.
+            // (Resetting them at the next group's start, after a wait only by et == 0, let a
+            // slow warp of the set still in this loop read a zeroed count and skip clearing --
+            // and exporting -- that pool's mask rows: a rare, timing-dependent wrong graph.)
+            tc::named_bar(bar_id, 96);
+            if (et < GP) sm.cl_n[b][et] = 0;
             tc::warp_arrive(&sm.mempty[m]);
         }
     }

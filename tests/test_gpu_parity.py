@@ -385,3 +385,22 @@ def test_init_dists_and_merge_messages_bit_exact(K, golden):
         m = (np.arange(cap)[None, :] < mc[:, None]).ravel()
         assert np.array_equal(mt[m], wt[m]) and np.array_equal(mi[m], wi[m]) and np.array_equal(md[m], wd[m])
         assert np.all(mt[~m] == -7)  # untouched tails
+
+
+def test_message_capacity_overflow_rebuilds_exactly(g, monkeypatch):
+    """build() starts with an optimistic message capacity; a round that outgrows it is
+    detected on the device (GRNND_ST_LOST) and the build is redone at the worst-case
+    capacity -- the graph is still the oracle's."""
+    from paper_2510_02774_b200 import builder as B
+
+    calls = []
+
+    def tiny(rows, cap):
+        calls.append(rows)
+        return 300
+
+    monkeypatch.setattr(B, "optimistic_msg_capacity", tiny)
+    ds = generate(3000, 32, "gaussian", seed=4)
+    graph = g.build(ds, g.BuildParams(S=12, R=24, T1=2, T2=3, rho=0.6, seed=4))
+    off, nb = oracle.build(ds.data, 12, 24, 2, 3, 0.6, 4)
+    assert calls and np.array_equal(graph.offsets, off) and np.array_equal(graph.neighbor_ids, nb)
