@@ -367,8 +367,7 @@ __global__ void __launch_bounds__(THREADS) pairs_kernel(PropArgs a, int bin, int
             if (v < 0) continue;
             const int k = sm.k[cur][g];
             const int ncl = sm.cl_n[g];
-            const int lcap = list_cap(cap);
-            if (ncl > lcap) {  // incomplete list: the masks go to global too
+            if (ncl > S::CL) {  // incomplete list: the masks go to global too
                 uint64_t *gc = a.w.cond + v * (int64_t)cap * mw;
                 uint64_t *ga = a.w.afar + v * (int64_t)cap * mw;
                 for (int e = tid; e < (k - 1) * mw; e += THREADS) {
@@ -377,9 +376,9 @@ __global__ void __launch_bounds__(THREADS) pairs_kernel(PropArgs a, int bin, int
                     ga[e] = wd < W ? sm.afar[g][x * W + wd] : 0ull;
                 }
             }
-            const int nw = ncl < lcap ? ncl : lcap;
+            const int nw = ncl < S::CL ? ncl : S::CL;
             int32_t *rec = a.w.clrec + v * (int64_t)CLREC;
-            if (tid == 0) a.w.clcnt[v] = ncl;
+            if (tid == 0) a.w.clcnt[v] = nw | (ncl > S::CL ? CL_TRUNC : 0);
             for (int e = tid; e < nw; e += THREADS) {
                 rec[4 + 2 * e] = (int32_t)sm.cl_key[g][e];
                 rec[5 + 2 * e] = __float_as_int(sm.cl_d[g][e]);

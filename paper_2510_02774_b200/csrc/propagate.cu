@@ -276,6 +276,7 @@ struct DecideSmem {
     int16_t e_id[DEC_WARPS][CAPM];
     uint16_t e_key[DEC_WARPS][CAPM];  // (anchor pos << 8) | partner pos of message j
     float e_d[DEC_WARPS][CAPM];       // kept exact distance of message j (NaN bits: not kept)
+    int2 rec[DEC_WARPS][PAIR_LIST];   // the pool's kept records (key, distance bits)
     uint64_t bm[DEC_WARPS][32][MW];   // cond / afar words of the current 32-anchor block
     uint64_t bf[DEC_WARPS][32][MW];
 };
@@ -460,14 +461,14 @@ __global__ void __launch_bounds__(dec_warps<MW>() * 32, 4) decide_kernel(PropArg
     for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
         const int k = a.read_count[v];
         if (k < 2) continue;  // no pairs (slice-mode survivors of k <= 1 come from bin_kernel)
-        const int ncl_all = a.w.clcnt[v];
-        if (!a.slice_mode && ncl_all == 0) {
+        const int32_t clc = a.w.clcnt[v];
+        if (!a.slice_mode && clc == 0) {
             // no redirect-capable pair: nothing is emitted or tombstoned (survivors stay in the
             // row, which the round API keeps packed), and the reference visits every pair
             if (lane == 0) refp_total += (unsigned long long)k * (unsigned long long)(k - 1) / 2ull;
             continue;
         }
-        recpools += ncl_all > 0 ? 1ull : 0ull;
+        recpools += clc != 0 ? 1ull : 0ull;
         for (int s = lane; s < k; s += 32) {
             ids[s] = a.read_ids[v * cap + s];
             pos[s] = a.w.pos8[v * a.w.pcap + s];
@@ -475,15 +476,12 @@ __global__ void __launch_bounds__(dec_warps<MW>() * 32, 4) decide_kernel(PropArg
         const uint64_t *gc = a.w.cond + v * (int64_t)cap * MW;
         const uint64_t *ga = a.w.afar + v * (int64_t)cap * MW;
         // redirect-capable pairs (workspace.cuh PAIR_LIST): a complete list replaces the masks
-        const int lcap = list_cap(cap);
+        const bool from_list = (clc & CL_TRUNC) == 0;
+        const int ncl = clc & (CL_TRUNC - 1);
         const int32_t *rec = a.w.clrec + v * (int64_t)CLREC;
-        const bool from_list = ncl_all <= lcap;
-        const int ncl = ncl_all < lcap ? ncl_all : lcap;
-        int2 e0 = make_int2(0, 0), e1 = make_int2(0, 0);
-        if (lane < ncl) e0 = *reinterpret_cast<const int2 *>(rec + 4 + 2 * lane);
-        if (lane + 32 < ncl) e1 = *reinterpret_cast<const int2 *>(rec + 4 + 2 * (lane + 32));
-        const uint32_t key0 = (uint32_t)e0.x, key1 = (uint32_t)e1.x;
-        const float cd0 = __int_as_float(e0.y), cd1 = __int_as_float(e1.y);
+        int2 *srec = sm.rec[wib];  // staged in shared memory (registers would spill)
+        for (int t = lane; t < ncl; t += 32) srec[t] = *reinterpret_cast<const int2 *>(rec + 4 + 2 * t);
+        __syncwarp();
         uint64_t(*bm)[MW] = sm.bm[wib];
         uint64_t(*bf)[MW] = sm.bf[wib];
         // a complete list: each lane ORs its (<= 2) records of the current anchor block into
@@ -494,10 +492,9 @@ __global__ void __launch_bounds__(dec_warps<MW>() * 32, 4) decide_kernel(PropArg
 #pragma unroll
                 for (int i = 0; i < MW; ++i) bm[lane][i] = bf[lane][i] = 0ull;
                 __syncwarp();
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const uint32_t kk = h ? key1 : key0;
-                    if (lane + 32 * h < ncl) {
+                for (int t = lane; t < ncl; t += 32) {
+                    const uint32_t kk = (uint32_t)srec[t].x;
+                    {
                         const int xr = (int)((kk >> 8) & 255u) - x0, xb = (int)(kk & 255u);
                         if (xr >= 0 && xr < 32) {
                             const uint64_t bit = 1ull << (xb & 63);
@@ -530,8 +527,8 @@ __global__ void __launch_bounds__(dec_warps<MW>() * 32, 4) decide_kernel(PropArg
                 __syncwarp();
                 for (int t = 0; t < nm; ++t) {
                     const uint32_t et = ek[t];
-                    if (lane < ncl && (key0 & 0xFFFFu) == et) e_d[t] = cd0;
-                    if (lane + 32 < ncl && (key1 & 0xFFFFu) == et) e_d[t] = cd1;
+                    for (int h = lane; h < ncl; h += 32)
+                        if (((uint32_t)srec[h].x & 0xFFFFu) == et) e_d[t] = __int_as_float(srec[h].y);
                 }
                 __syncwarp();
             }

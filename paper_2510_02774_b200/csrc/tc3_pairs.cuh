@@ -637,13 +637,12 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             tc::warp_arrive(&sm.empty[s]);
             // pair records -> global (decide_kernel); masks only for incomplete
             // lists (rare; regular stores); every mask row re-zeroed for the next group
-            const int lcap = list_cap(cap);
             if (et < GP && mt.hdr[et].x >= 0) {
                 const int c = sm.cl_n[b][et];
                 sm.rec[b][et][0] = c;
                 tc::fence_proxy_async();  // the header, for the bulk store issued by et == 0
                 if (c > 0) {  // the counts were zeroed for the round
-                    a.w.clcnt[mt.hdr[et].x] = c;
+                    a.w.clcnt[mt.hdr[et].x] = (c < S::CL ? c : S::CL) | (c > S::CL ? CL_TRUNC : 0);
                     st_red += (unsigned long long)c;
                 }
             }
@@ -655,7 +654,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 const uint64_t cv = sm.cond[b][r][wd], fv = sm.afar[b][r][wd];
                 sm.cond[b][r][wd] = 0ull;
                 sm.afar[b][r][wd] = 0ull;
-                if (v >= 0 && wd < mw && x < mt.hdr[pp].y - 1 && sm.cl_n[b][pp] > lcap) {
+                if (v >= 0 && wd < mw && x < mt.hdr[pp].y - 1 && sm.cl_n[b][pp] > S::CL) {
                     a.w.cond[(v * cap + x) * mw + wd] = cv;
                     a.w.afar[(v * cap + x) * mw + wd] = fv;
                 }
@@ -669,7 +668,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 for (int pp = 0; pp < GP; ++pp) {
                     const int64_t v = mt.hdr[pp].x;
                     if (v < 0 || sm.cl_n[b][pp] == 0) continue;  // no records: nothing to store
-                    const int nw = sm.cl_n[b][pp] < lcap ? sm.cl_n[b][pp] : lcap;
+                    const int nw = sm.cl_n[b][pp] < S::CL ? sm.cl_n[b][pp] : S::CL;
                     const uint32_t bytes = (uint32_t)((16 + 8 * nw + 15) & ~15);
                     tc::fence_proxy_async();
                     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(

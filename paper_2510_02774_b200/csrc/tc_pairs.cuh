@@ -139,7 +139,7 @@ template <int SZ>
 struct TcSmem {
     static constexpr int GP = 128 / SZ;  // pools per group
     static constexpr int NM = 4;         // metadata slots
-    static constexpr int CL = PAIR_LIST;  // redirect-capable pairs handed to decide (workspace.cuh)
+    static constexpr int CL = 64;  // redirect-capable pairs handed to decide (<= PAIR_LIST, workspace.cuh)
     static constexpr int QC = 1024;      // filter candidates per group (overflow: exact sweep)
     int32_t ids[NM][128];
     float dv[NM][128];
@@ -411,7 +411,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_pairs_kernel(PropArgs a, int
         }
         __syncthreads();  // masks + kept distances complete
         // ---- kept pairs -> global (decide_kernel); masks only for incomplete lists; re-zero ----
-        const int lcap = list_cap(cap);
         for (int e = tid; e < 128 * mw; e += NT) {
             const int r = mw == 2 ? e >> 1 : e, wd = mw == 2 ? e & 1 : 0;  // group row = p * SZ + anchor pos
             const int pp = r / SZ, x = r - pp * SZ;
@@ -424,7 +423,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_pairs_kernel(PropArgs a, int
                 sm.cond[r][wd] = 0ull;
                 sm.afar[r][wd] = 0ull;
             }
-            if (sm.cl_n[qs][pp] > lcap) {
+            if (sm.cl_n[qs][pp] > S::CL) {
                 a.w.cond[(v * cap + x) * mw + wd] = cv;
                 a.w.afar[(v * cap + x) * mw + wd] = fv;
             }
@@ -434,10 +433,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_pairs_kernel(PropArgs a, int
             const int64_t v = sm.v[ms][pp];
             if (v < 0) continue;
             const int ncl = sm.cl_n[qs][pp];
-            const int nw = ncl < lcap ? ncl : lcap;
+            const int nw = ncl < S::CL ? ncl : S::CL;
             int32_t *rec = a.w.clrec + v * (int64_t)CLREC;
             if (c == 0) {
-                a.w.clcnt[v] = ncl;
+                if (ncl > 0) a.w.clcnt[v] = nw | (ncl > S::CL ? CL_TRUNC : 0);
                 red_local += (unsigned long long)ncl;
             }
             if (c < nw) {

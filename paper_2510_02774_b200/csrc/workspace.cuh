@@ -10,14 +10,16 @@ namespace grnnd {
 constexpr int NBINS = 8;  // propagate bins by live count k: see propagate.cu
 constexpr int HEAVY_SEG = 32;  // segments longer than this are sorted by a CTA
 // Redirect-capable pairs of a pool, as the pair phase hands them to decide_kernel: one
-// record of CLREC int32 per vertex: [0] = their count, [4 + 2c] = (afar << 16) | (anchor pos
-// << 8) | partner pos and [5 + 2c] = the pair's exact distance (fp32 bits) for c < min(count,
-// list_cap(cap)).  A complete list is all decide needs; only when count > list_cap are the
-// full cond / afar masks written as well.  (16-byte aligned records: bulk-stored by tc3.)
+// record of CLREC int32 per vertex: [4 + 2c] = (afar << 16) | (anchor pos << 8) | partner
+// pos and [5 + 2c] = the pair's exact distance (fp32 bits) for the c < stored count kept;
+// clcnt[v] = stored count | CL_TRUNC when the pair kernel found more pairs than its list
+// holds (its shared-memory list: <= PAIR_LIST).  A complete list is all decide needs; for an
+// incomplete one the full cond / afar masks are written too and decide re-evaluates the
+// distances the list lacks.  (16-byte aligned records: bulk-stored by tc3.)
 constexpr int PAIR_LIST = 64;
+constexpr int32_t CL_TRUNC = 1 << 30;
 constexpr int T3_META_REC = 1344;  // sizeof(T3Meta): 96 x (id, dv, norm: 4 B; pos: 1 B) + 12 x int2
 constexpr int CLREC = 4 + 2 * PAIR_LIST;
-__host__ __device__ inline int list_cap(int cap) { return PAIR_LIST < 4 * cap ? PAIR_LIST : 4 * cap; }
 
 // small counters block (unsigned long long so atomicAdd works on it)
 enum Counter : int {
@@ -61,7 +63,7 @@ struct Workspace {
     uint64_t *cond;      // [n, cap, mw] redirect-condition bits, row = anchor position
     uint64_t *afar;      // [n, cap, mw] "anchor is the farther member" bits
     int32_t *clrec;      // [n, CLREC] redirect-capable pair records (see PAIR_LIST)
-    int32_t *clcnt;      // [n] their count this round (zeroed per round; the tc3 path writes non-zero only)
+    int32_t *clcnt;      // [n] stored count | CL_TRUNC (zeroed per round; written for pools with records only)
     // tensor-core pair phase (tc3_pairs.cuh): one T3_META_REC-byte metadata record per
     // group of 96 slots -- pool ids, stored distances, row norms, positions, (vertex, k) per
     // pool -- fetched by ONE bulk copy (only carved when cap <= 96)
