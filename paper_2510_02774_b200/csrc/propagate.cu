@@ -639,16 +639,20 @@ static int launch_tc_pairs(const PropArgs &a, int bin, cudaStream_t st) {
 
 template <int SZ>
 static int launch_tc3_pairs(const PropArgs &a, int bin, cudaStream_t st) {
-    auto kern = tc3_pairs_kernel<SZ>;
+    const bool multi = a.dim > 128;
+    auto kern = multi ? tc3_pairs_kernel<SZ, true> : tc3_pairs_kernel<SZ, false>;
     const size_t smem = (size_t)T3_NS * T3_STAGE + T3_PAD + sizeof(T3Smem<SZ>) + 1024;
-    static SmemOptIn optin;
-    GRNND_CUDA(optin.ensure(kern, smem));
+    static SmemOptIn optin[2];  // one per kernel
+    GRNND_CUDA(optin[multi ? 1 : 0].ensure(kern, smem));
     kern<<<device_sm_count(), T3_NT, smem, st>>>(a, bin);
     return check_launch("tc3_pairs_kernel");
 }
 
 #ifndef GRNND_TC
 #define GRNND_TC 1  // tensor-core Gram pre-screen (tc_pairs.cuh) for D <= 128, R <= 128
+#endif
+#ifndef GRNND_TC_MULTI
+#define GRNND_TC_MULTI 1  // ... and for D > 128 with R <= 96 (tc3 MULTI)
 #endif
 
 
@@ -657,7 +661,9 @@ int launch_propagate(const PropArgs &a, cudaStream_t st) {
     if (n <= 0) return GRNND_OK;
     GRNND_CUDA(cudaMemsetAsync(a.w.ctr + C_BIN0, 0, sizeof(unsigned long long) * NBINS, st));
     GRNND_CUDA(cudaMemsetAsync(a.w.clcnt, 0, sizeof(int32_t) * (size_t)n, st));
-    const bool tc3 = GRNND_TC && a.norms && a.dim <= 128 && a.cap <= T3_ROWS && a.order_code == 0;
+    // tensor-core pair phase: D <= 128 stages whole rows; D > 128 streams 128-dim chunks
+    // through the same pipeline (tc3_pairs.cuh, MULTI)
+    const bool tc3 = GRNND_TC && a.norms && (a.dim <= 128 || GRNND_TC_MULTI) && a.cap <= T3_ROWS && a.order_code == 0;
     const int tb = 128;
     {
         static SmemOptIn optin;

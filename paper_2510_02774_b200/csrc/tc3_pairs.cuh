@@ -143,7 +143,11 @@ __device__ long long g_t3trace[64][10];  // CTA 0: per group event times (profil
 #define GRNND_T3_NOFILTER 0  // timing experiment only (results invalid): the filter queues nothing
 #endif
 
-template <int SZ>
+// MULTI (D > 128): each group's rows stream through the stage ring as ceil(D / 128) chunks of
+// 128 dims; the MMA accumulates the chunks' Grams in the same TMEM accumulator and releases
+// each stage with tcgen05.commit (the exact sets never hold a stage); the exact chains read
+// the candidate pairs' rows from global memory (L2: the group's rows were just streamed).
+template <int SZ, bool MULTI>
 __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin) {
     using S = T3Smem<SZ>;
     constexpr int GP = S::GP;
@@ -167,6 +171,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
     const int64_t nmine = (ngroups - blockIdx.x + G - 1) / G;
     const int64_t gbase = tc_group_base(a.w.ctr, bin);
     const int nq = (a.dim + 3) >> 2;
+    const int nch = MULTI ? (nq + 31) >> 5 : 1;  // 128-dim chunks per group
     const int cap = a.cap, mw = a.w.mw;
     unsigned long long st_pairs = 0, st_cand = 0, st_ovf = 0, st_red = 0;
 
@@ -183,7 +188,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
 #else
             tc::mbar_init(&sm.full[s], T3_NP * 32);
 #endif
-            tc::mbar_init(&sm.empty[s], 3);
+            tc::mbar_init(&sm.empty[s], MULTI ? 1 : 3);  // MULTI: the MMA's commit frees a stage
         }
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&sm.accf[b], 1);
@@ -226,62 +231,77 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
         // warp pi stages group rows pi, pi + 9, ..: one 512-byte row per instruction (lane =
         // 16-byte chunk, 128-byte swizzle)
         const int pi = warp - 11;
-        const bool cv = lane < nq;
         const uint32_t lo = (uint32_t)((lane >> 3) * T3_KB), lx = (uint32_t)(lane & 7);
         for (int64_t g = 0; g < nmine; ++g) {
-            const int s = (int)(g % NS), m = (int)(g % NM);
+            const int m = (int)(g % NM);
             T3P_WAIT(15, tc::mbar_wait(&sm.mfull[m], (uint32_t)((g / NM) & 1)));
-            T3P_WAIT(16, tc::mbar_wait(&sm.empty[s], (uint32_t)(((g / NS) & 1) ^ 1)));
-            const uint32_t stg = tc::smem_u32(base + s * T3_STAGE);
+            for (int c = 0; c < nch; ++c) {
+                const int64_t u = g * nch + c;  // stage use index
+                const int s = (int)(u % NS);
+                const bool cv = c * 32 + lane < nq;
+                T3P_WAIT(16, tc::mbar_wait(&sm.empty[s], (uint32_t)(((u / NS) & 1) ^ 1)));
+                const uint32_t stg = tc::smem_u32(base + s * T3_STAGE);
 #pragma unroll
-            for (int q = 0; q < (R + T3_NP - 1) / T3_NP; ++q) {
-                const int r = pi + T3_NP * q;
-                if (r >= R) break;
-                const int32_t id = sm.meta[m].ids[r];
-                if (id == TOMB) continue;  // empty slot (warp-uniform)
-                const float *src = a.data + (int64_t)id * a.ld + (cv ? lane * 4 : 0);
-                const uint32_t dst = stg + lo + (uint32_t)((r >> 3) * 1024 + (r & 7) * 128) + ((lx ^ (uint32_t)(r & 7)) << 4);
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(cv ? 16 : 0));
-            }
-            if (pi == 0 && lane == 0) T3P_EV(g, 1);
+                for (int q = 0; q < (R + T3_NP - 1) / T3_NP; ++q) {
+                    const int r = pi + T3_NP * q;
+                    if (r >= R) break;
+                    const int32_t id = sm.meta[m].ids[r];
+                    if (id == TOMB) continue;  // empty slot (warp-uniform)
+                    const float *src = a.data + (int64_t)id * a.ld + (cv ? (c * 32 + lane) * 4 : 0);
+                    const uint32_t dst = stg + lo + (uint32_t)((r >> 3) * 1024 + (r & 7) * 128) + ((lx ^ (uint32_t)(r & 7)) << 4);
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(cv ? 16 : 0));
+                }
+                if (pi == 0 && lane == 0 && c == 0) T3P_EV(g, 1);
 #ifdef GRNND_T3_PROF
-            if (lane == 0 && blockIdx.x == 0 && g < 64) atomicMax((unsigned long long *)&g_t3trace[g][2], (unsigned long long)clock64());
+                if (lane == 0 && blockIdx.x == 0 && g < 64 && c == 0) atomicMax((unsigned long long *)&g_t3trace[g][2], (unsigned long long)clock64());
 #endif
-            // one arrive per lane, performed by the hardware when the lane's copies have landed;
-            // the MMA thread fences the async proxy before the tensor core reads the stage
+                // one arrive per lane, performed by the hardware when the lane's copies have landed;
+                // the MMA thread fences the async proxy before the tensor core reads the stage
 #ifdef GRNND_T3_WAITGROUP
-            cp_async_commit();
-            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-            tc::fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&sm.full[s]);
+                cp_async_commit();
+                asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+                tc::fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&sm.full[s]);
 #else
-            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&sm.full[s])) : "memory");
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&sm.full[s])) : "memory");
 #endif
+            }
         }
     } else if (warp == 1) {
         // ================= MMA issuer =================
         if (lane == 0) {
             for (int64_t g = 0; g < nmine; ++g) {
-                const int s = (int)(g % NS), m = (int)(g % NM), ac = (int)(g & 1);
-                T3P_WAIT(2, tc::mbar_wait(&sm.full[s], (uint32_t)((g / NS) & 1)));
-                T3P_EV(g, 0);  // (overrides "meta issued"): rows landed, as seen by the MMA thread
-                tc::mbar_wait(&sm.mfull[m], (uint32_t)((g / NM) & 1));
-                T3P_WAIT(3, tc::mbar_wait(&sm.acce[ac], (uint32_t)(((g >> 1) & 1) ^ 1)));
-                T3P_WAIT(20, tc::fence_after(); tc::fence_proxy_async());  // cp.async (generic proxy) writes -> tensor core reads
-                const int n = GP == 1 ? ((sm.meta[m].hdr[0].y + 15) / 16 * 16) : R;
-                const uint32_t idesc = tc::idesc_tf32(n < 16 ? 16 : n);
-                const uint32_t sa = tc::smem_u32(base + s * T3_STAGE);
+                const int m = (int)(g % NM), ac = (int)(g & 1);
                 const uint32_t d = tmem + (uint32_t)(ac * 128);
-#pragma unroll
-                for (int kb = 0; kb < 4; ++kb)
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        const uint64_t desc = tc::sw128_desc(sa + kb * T3_KB + kk * 32);
-#ifndef GRNND_T3_NOMMA
-                        tc::mma_tf32(d, desc, desc, idesc, (kb | kk) != 0);
-#endif
+                for (int c = 0; c < nch; ++c) {
+                    const int64_t u = g * nch + c;
+                    const int s = (int)(u % NS);
+                    T3P_WAIT(2, tc::mbar_wait(&sm.full[s], (uint32_t)((u / NS) & 1)));
+                    if (c == 0) {
+                        T3P_EV(g, 0);  // (overrides "meta issued"): rows landed, as seen by the MMA thread
+                        tc::mbar_wait(&sm.mfull[m], (uint32_t)((g / NM) & 1));
+                        T3P_WAIT(3, tc::mbar_wait(&sm.acce[ac], (uint32_t)(((g >> 1) & 1) ^ 1)));
                     }
+                    T3P_WAIT(20, tc::fence_after(); tc::fence_proxy_async());  // cp.async (generic proxy) writes -> tensor core reads
+                    const int n = GP == 1 ? ((sm.meta[m].hdr[0].y + 15) / 16 * 16) : R;
+                    const uint32_t idesc = tc::idesc_tf32(n < 16 ? 16 : n);
+                    const uint32_t sa = tc::smem_u32(base + s * T3_STAGE);
+                    // k-blocks of 32 dims holding data (a short last chunk: fewer; the rest is 0)
+                    const int kbn = MULTI ? min(4, (nq - c * 32 + 7) >> 3) : 4;
+#pragma unroll
+                    for (int kb = 0; kb < 4; ++kb) {
+                        if (kb >= kbn) break;
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) {
+                            const uint64_t desc = tc::sw128_desc(sa + kb * T3_KB + kk * 32);
+#ifndef GRNND_T3_NOMMA
+                            tc::mma_tf32(d, desc, desc, idesc, (c | kb | kk) != 0);
+#endif
+                        }
+                    }
+                    if (MULTI) tc::mma_commit(&sm.empty[s]);  // the stage is free once these MMAs have read it
+                }
                 T3P_EV(g, 3);
                 T3P_WAIT(21, tc::mma_commit(&sm.accf[ac]));
             }
@@ -382,8 +402,11 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                         const int jr = cb + c, ii = tr ? jr : i, jj = tr ? i : jr;
                         float dx = 0.0f;
                         for (int q = 0; q < nq; ++q) {
-                            const float4 x = *reinterpret_cast<const float4 *>(stg + t3_off(ii, q));
-                            const float4 y = *reinterpret_cast<const float4 *>(stg + t3_off(jj, q));
+                            // (MULTI: the group's rows are no longer staged: from global memory)
+                            const float4 x = MULTI ? __ldg(reinterpret_cast<const float4 *>(a.data + (int64_t)mt.ids[ii] * a.ld) + q)
+                                                   : *reinterpret_cast<const float4 *>(stg + t3_off(ii, q));
+                            const float4 y = MULTI ? __ldg(reinterpret_cast<const float4 *>(a.data + (int64_t)mt.ids[jj] * a.ld) + q)
+                                                   : *reinterpret_cast<const float4 *>(stg + t3_off(jj, q));
                             dx = exact_step(dx, x.x, y.x);
                             dx = exact_step(dx, x.y, y.y);
                             dx = exact_step(dx, x.z, y.z);
@@ -522,8 +545,106 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                     sm.rec[b][p][5 + 2 * c] = __float_as_int(d);
                 }
             };
-            // this thread's queue entries to registers, then hand the queue back to the filter
             const int qn = sm.qn[b];
+#ifdef GRNND_T3_PROF
+            const long long _tx0 = clock64();
+#endif
+            if constexpr (MULTI) {
+                // D > 128: the exact chains read the rows from global memory.  Two pairs per
+                // warp: the lanes square 16-byte chunks of the four rows, 128 dims at a time (the
+                // next chunk's loads issued before this chunk's sums), lanes 0 / 1 add the
+                // squares in the reference's order.  The queue is read in place and handed back
+                // to the filter afterwards (the filter is not this path's bottleneck).
+                if (et == 0) {
+                    st_cand += (unsigned long long)qn;
+                    st_ovf += qn > S::QC ? 1ull : 0ull;
+                }
+                const int ew = et >> 5;
+                float *ps = &sm.psq[E * 3 + ew][0][0];
+                auto coop2 = [&](int i1, int j1, int i2, int j2, float &x1, float &x2) {
+                    auto row = [&](int r) {
+                        const int32_t id = mt.ids[r];
+                        return reinterpret_cast<const float4 *>(a.data + (int64_t)(id < 0 ? 0 : id) * a.ld);
+                    };
+                    const float4 *ra = row(i1), *rb = row(j1), *rc = row(i2), *rd = row(j2);
+                    float4 p1, p2;
+                    auto sq = [&](int c) {
+                        const int q = c * 32 + lane;
+                        if (q < nq) {
+                            const float4 x = __ldg(ra + q), y = __ldg(rb + q), z = __ldg(rc + q), w = __ldg(rd + q);
+                            p1 = make_float4(exact_step(0.f, x.x, y.x), exact_step(0.f, x.y, y.y), exact_step(0.f, x.z, y.z),
+                                             exact_step(0.f, x.w, y.w));
+                            p2 = make_float4(exact_step(0.f, z.x, w.x), exact_step(0.f, z.y, w.y), exact_step(0.f, z.z, w.z),
+                                             exact_step(0.f, z.w, w.w));
+                        } else {
+                            p1 = p2 = make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+                    };
+                    sq(0);
+                    float acc = 0.0f;
+                    for (int c = 0; c < nch; ++c) {
+                        reinterpret_cast<float4 *>(ps)[lane] = p1;
+                        reinterpret_cast<float4 *>(ps + 128)[lane] = p2;
+                        __syncwarp();
+                        if (c + 1 < nch) sq(c + 1);
+                        if (lane < 2) {
+                            const float4 *pv = reinterpret_cast<const float4 *>(ps + 128 * lane);
+                            const int nc = nq - c * 32 < 32 ? nq - c * 32 : 32;
+#pragma unroll 8
+                            for (int cc = 0; cc < nc; ++cc) {
+                                const float4 v = pv[cc];
+                                acc = __fadd_rn(acc, v.x);
+                                acc = __fadd_rn(acc, v.y);
+                                acc = __fadd_rn(acc, v.z);
+                                acc = __fadd_rn(acc, v.w);
+                            }
+                        }
+                        __syncwarp();
+                    }
+                    x1 = __shfl_sync(FULL, acc, 0);
+                    x2 = __shfl_sync(FULL, acc, 1);
+                };
+                auto keep = [&](int i, int j, float x) {
+                    const float av = mt.dv[i], bv = mt.dv[j];
+                    if (mt.ids[i] != TOMB && mt.ids[j] != TOMB && x < (av >= bv ? av : bv)) record(i, j, x);
+                };
+                if (qn <= S::QC) {
+                    for (int e = ew * 2; e < qn; e += 6) {  // warp-uniform: queue entries e, e + 1
+                        const bool two = e + 1 < qn;
+                        const uint32_t k1 = sm.q[b][e], k2 = sm.q[b][two ? e + 1 : e];
+                        const int i1 = (int)(k1 >> 8), j1 = (int)(k1 & 255u), i2 = (int)(k2 >> 8), j2 = (int)(k2 & 255u);
+                        float x1, x2;
+                        coop2(i1, j1, i2, j2, x1, x2);
+                        if (lane == 0) {
+                            keep(i1, j1, x1);
+                            if (two) keep(i2, j2, x2);
+                        }
+                    }
+                } else {
+                    // queue overflow (degenerate data): every pair of every pool
+                    for (int pp = 0; pp < GP; ++pp) {
+                        const int k = mt.hdr[pp].x >= 0 ? mt.hdr[pp].y : 0;
+                        const int npairs = k * (k - 1) / 2;
+                        for (int t = ew * 2; t < npairs; t += 6) {
+                            const bool two = t + 1 < npairs;
+                            int s1, u1, s2 = 0, u2 = 0;
+                            tile_decode(t, s1, u1);
+                            if (two) tile_decode(t + 1, s2, u2);
+                            const int i1 = pp * SZ + s1, j1 = pp * SZ + u1 + 1;
+                            const int i2 = two ? pp * SZ + s2 : i1, j2 = two ? pp * SZ + u2 + 1 : j1;
+                            float x1, x2;
+                            coop2(i1, j1, i2, j2, x1, x2);
+                            if (lane == 0) {
+                                keep(i1, j1, x1);
+                                if (two) keep(i2, j2, x2);
+                            }
+                        }
+                    }
+                }
+                tc::warp_arrive(&sm.qemp[b]);
+                if (et == 0) T3P_EV(g, 6);
+            } else {
+            // this thread's queue entries to registers, then hand the queue back to the filter
             const uint32_t qw = (qn <= 32 && lane < qn) ? sm.q[b][lane] : 0u;  // short queues: per warp
             constexpr int QT = (S::QC + NE - 1) / NE;
             uint32_t qk[QT + (QT & 1)];
@@ -534,9 +655,6 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             }
             tc::warp_arrive(&sm.qemp[b]);
             if (et == 0) T3P_EV(g, 6);
-#ifdef GRNND_T3_PROF
-            const long long _tx0 = clock64();
-#endif
             if (et == 0) {
                 st_cand += (unsigned long long)qn;
                 st_ovf += qn > S::QC ? 1ull : 0ull;
@@ -622,6 +740,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                     }
                 }
             }
+            }  // !MULTI
 #ifdef GRNND_T3_PROF
             if (lane == 0) T3P_ADD(18, _tx0);
 #endif
@@ -633,8 +752,9 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
 #ifdef GRNND_T3_PROF
             const long long _tx1 = clock64();
 #endif
-            // the stage's rows are no longer read: let the producers refill it
-            tc::warp_arrive(&sm.empty[s]);
+            // the stage's rows are no longer read: let the producers refill it (MULTI: the MMA
+            // released the group's stages)
+            if (!MULTI) tc::warp_arrive(&sm.empty[s]);
             // pair records -> global (decide_kernel); masks only for incomplete
             // lists (rare; regular stores); every mask row re-zeroed for the next group
             if (et < GP && mt.hdr[et].x >= 0) {

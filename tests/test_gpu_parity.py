@@ -404,3 +404,16 @@ def test_message_capacity_overflow_rebuilds_exactly(g, monkeypatch):
     graph = g.build(ds, g.BuildParams(S=12, R=24, T1=2, T2=3, rho=0.6, seed=4))
     off, nb = oracle.build(ds.data, 12, 24, 2, 3, 0.6, 4)
     assert calls and np.array_equal(graph.offsets, off) and np.array_equal(graph.neighbor_ids, nb)
+
+
+@pytest.mark.parametrize("dim,R", [(960, 96), (300, 48), (129, 24)])
+def test_tensor_core_multichunk_bit_exact(g, monkeypatch, dim, R):
+    """D > 128 on the tensor cores (tc3 MULTI: 128-dim chunks accumulated in TMEM, exact
+    chains from global rows), from round 1 (queue overflows -> exact sweeps) and after the
+    exact first rounds: the oracle's graph bit for bit."""
+    ds = generate(3000, dim, "gaussian", seed=dim)
+    off, nb = oracle.build(ds.data, 16, R, 2, 4, 0.6, 5)
+    for first in ("0", "3"):
+        monkeypatch.setenv("GRNND_EXACT_FIRST_ROUNDS", first)
+        graph = g.build(ds, g.BuildParams(S=16, R=R, T1=2, T2=4, rho=0.6, seed=5))
+        assert np.array_equal(graph.offsets, off) and np.array_equal(graph.neighbor_ids, nb), (dim, R, first)

@@ -43,6 +43,7 @@ def run_tcv(*args):
     (20000, 128, 128, 2, 6, "gaussian"),   # 96 < R <= 128: the tc_pairs path
     (8000, 100, 112, 2, 5, "clustered"),
     (6000, 64, 40, 2, 5, "uniform"),
+    (4000, 960, 96, 2, 5, "gaussian"),     # D > 128: chunked Gram accumulated over K = 960
 ])
 def test_tensor_core_bound_holds_and_graph_exact(n, dim, R, T1, T2, dist):
     r = run_tcv(n, dim, R, T1, T2, dist)
