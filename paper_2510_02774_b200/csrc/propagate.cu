@@ -640,8 +640,12 @@ static int launch_tc_pairs(const PropArgs &a, int bin, cudaStream_t st) {
 template <int SZ>
 static int launch_tc3_pairs(const PropArgs &a, int bin, cudaStream_t st) {
     const bool multi = a.dim > 128;
+    if (multi && device_sm_count() > T3Q_CTAS) {
+        set_error("tc3: %d SMs > %d overflow-queue slots", device_sm_count(), T3Q_CTAS);
+        return GRNND_EUNSUPPORTED;
+    }
     auto kern = multi ? tc3_pairs_kernel<SZ, true> : tc3_pairs_kernel<SZ, false>;
-    const size_t smem = (size_t)T3_NS * T3_STAGE + T3_PAD + sizeof(T3Smem<SZ>) + 1024;
+    const size_t smem = (size_t)T3_NS * T3_STAGE + T3_PAD + (multi ? sizeof(T3Smem<SZ, true>) : sizeof(T3Smem<SZ, false>)) + 1024;
     static SmemOptIn optin[2];  // one per kernel
     GRNND_CUDA(optin[multi ? 1 : 0].ensure(kern, smem));
     kern<<<device_sm_count(), T3_NT, smem, st>>>(a, bin);

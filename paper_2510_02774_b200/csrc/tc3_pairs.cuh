@@ -63,7 +63,8 @@ struct alignas(16) T3Meta {  // one group's metadata (staged by tc_stage_kernel,
 constexpr uint32_t T3_META_BYTES = 3 * 4 * T3_ROWS + T3_ROWS + 96;
 static_assert(sizeof(T3Meta) == T3_META_BYTES && T3_META_BYTES == T3_META_REC, "metadata record layout");
 
-template <int SZ>
+
+template <int SZ, bool MULTI>
 struct T3Smem {
     static constexpr int GP = T3_ROWS / SZ;
     // redirect-capable pairs handed to decide (workspace.cuh); a pool of k <= SZ has at most
@@ -80,7 +81,10 @@ struct T3Smem {
     int cl_n[2][GP];
     int qn[2];
     uint32_t q[2][QC];            // (row i << 8) | row j
-    alignas(16) float psq[6][2][128];  // per exact warp: the squared differences of two pairs
+    // per exact warp: the squared differences of two pairs (MULTI: one 128-dim chunk; the
+    // second pair's row starts 132 floats in, so the two summing lanes read distinct banks)
+    static constexpr int PSQW = MULTI ? 2 * 132 : 2 * 128;
+    alignas(16) float psq[6 * PSQW];
     uint64_t mfull[T3_NM], mempty[T3_NM], full[T3_NS], empty[T3_NS], accf[2], acce[2], qrdy[2], qemp[2];
     uint32_t tmem_base;
 };
@@ -149,7 +153,7 @@ __device__ long long g_t3trace[64][10];  // CTA 0: per group event times (profil
 // the candidate pairs' rows from global memory (L2: the group's rows were just streamed).
 template <int SZ, bool MULTI>
 __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin) {
-    using S = T3Smem<SZ>;
+    using S = T3Smem<SZ, MULTI>;
     constexpr int GP = S::GP;
     constexpr int R = T3_ROWS;
     constexpr int NS = T3_NS;
@@ -353,6 +357,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             }
 #endif
             const float2 abi = sm.ab[b][i];
+            uint32_t *gq = a.w.t3q + ((int64_t)blockIdx.x * 2 + b) * T3Q_GROUP;  // MULTI: queue overflow
             const int kcols = GP == 1 ? mt.hdr[0].y : R;
             const uint32_t trow = tmem + ((uint32_t)(fw * 32) << 16) + (uint32_t)(b * 128);
             unsigned np = 0;
@@ -433,7 +438,9 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                         const int c = __ffs(cm) - 1;
                         cm &= cm - 1u;
                         const int jr = cb + c;
-                        if (qi < S::QC) sm.q[b][qi] = tr ? (uint32_t)((jr << 8) | i) : (uint32_t)((i << 8) | jr);
+                        const uint32_t key = tr ? (uint32_t)((jr << 8) | i) : (uint32_t)((i << 8) | jr);
+                        if (qi < S::QC) sm.q[b][qi] = key;
+                        else if (MULTI) gq[qi - S::QC] = key;  // (< T3Q_GROUP - QC beyond: all pairs fit)
                         ++qi;
                     }
                 }
@@ -560,13 +567,17 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                     st_ovf += qn > S::QC ? 1ull : 0ull;
                 }
                 const int ew = et >> 5;
-                float *ps = &sm.psq[E * 3 + ew][0][0];
-                auto coop2 = [&](int i1, int j1, int i2, int j2, float &x1, float &x2) {
+                float *ps = sm.psq + (E * 3 + ew) * S::PSQW;
+                // two pairs per warp (keys k1, k2: group rows (i << 8) | j): the lanes square
+                // 16-byte chunks of the four rows, 128 dims at a time (the next chunk's loads
+                // issued before this chunk's sums), lanes 0 / 1 add the squares in order
+                auto coop2 = [&](uint32_t k1, uint32_t k2, float &x1, float &x2) {
                     auto row = [&](int r) {
                         const int32_t id = mt.ids[r];
                         return reinterpret_cast<const float4 *>(a.data + (int64_t)(id < 0 ? 0 : id) * a.ld);
                     };
-                    const float4 *ra = row(i1), *rb = row(j1), *rc = row(i2), *rd = row(j2);
+                    const float4 *ra = row((int)(k1 >> 8)), *rb = row((int)(k1 & 255u));
+                    const float4 *rc = row((int)(k2 >> 8)), *rd = row((int)(k2 & 255u));
                     float4 p1, p2;
                     auto sq = [&](int c) {
                         const int q = c * 32 + lane;
@@ -584,11 +595,11 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                     float acc = 0.0f;
                     for (int c = 0; c < nch; ++c) {
                         reinterpret_cast<float4 *>(ps)[lane] = p1;
-                        reinterpret_cast<float4 *>(ps + 128)[lane] = p2;
+                        reinterpret_cast<float4 *>(ps + 132)[lane] = p2;
                         __syncwarp();
                         if (c + 1 < nch) sq(c + 1);
                         if (lane < 2) {
-                            const float4 *pv = reinterpret_cast<const float4 *>(ps + 128 * lane);
+                            const float4 *pv = reinterpret_cast<const float4 *>(ps + 132 * lane);
                             const int nc = nq - c * 32 < 32 ? nq - c * 32 : 32;
 #pragma unroll 8
                             for (int cc = 0; cc < nc; ++cc) {
@@ -604,41 +615,23 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                     x1 = __shfl_sync(FULL, acc, 0);
                     x2 = __shfl_sync(FULL, acc, 1);
                 };
-                auto keep = [&](int i, int j, float x) {
+                auto keep = [&](uint32_t kk, float x) {
+                    const int i = (int)(kk >> 8), j = (int)(kk & 255u);
                     const float av = mt.dv[i], bv = mt.dv[j];
                     if (mt.ids[i] != TOMB && mt.ids[j] != TOMB && x < (av >= bv ? av : bv)) record(i, j, x);
                 };
-                if (qn <= S::QC) {
-                    for (int e = ew * 2; e < qn; e += 6) {  // warp-uniform: queue entries e, e + 1
-                        const bool two = e + 1 < qn;
-                        const uint32_t k1 = sm.q[b][e], k2 = sm.q[b][two ? e + 1 : e];
-                        const int i1 = (int)(k1 >> 8), j1 = (int)(k1 & 255u), i2 = (int)(k2 >> 8), j2 = (int)(k2 & 255u);
-                        float x1, x2;
-                        coop2(i1, j1, i2, j2, x1, x2);
-                        if (lane == 0) {
-                            keep(i1, j1, x1);
-                            if (two) keep(i2, j2, x2);
-                        }
-                    }
-                } else {
-                    // queue overflow (degenerate data): every pair of every pool
-                    for (int pp = 0; pp < GP; ++pp) {
-                        const int k = mt.hdr[pp].x >= 0 ? mt.hdr[pp].y : 0;
-                        const int npairs = k * (k - 1) / 2;
-                        for (int t = ew * 2; t < npairs; t += 6) {
-                            const bool two = t + 1 < npairs;
-                            int s1, u1, s2 = 0, u2 = 0;
-                            tile_decode(t, s1, u1);
-                            if (two) tile_decode(t + 1, s2, u2);
-                            const int i1 = pp * SZ + s1, j1 = pp * SZ + u1 + 1;
-                            const int i2 = two ? pp * SZ + s2 : i1, j2 = two ? pp * SZ + u2 + 1 : j1;
-                            float x1, x2;
-                            coop2(i1, j1, i2, j2, x1, x2);
-                            if (lane == 0) {
-                                keep(i1, j1, x1);
-                                if (two) keep(i2, j2, x2);
-                            }
-                        }
+                // the queue: its first QC entries in shared memory, the rest in the CTA's global
+                // overflow buffer (written by the filter before its qrdy arrival)
+                const uint32_t *gqb = a.w.t3q + ((int64_t)blockIdx.x * 2 + b) * T3Q_GROUP;
+                auto qkey = [&](int e) { return e < S::QC ? sm.q[b][e] : gqb[e - S::QC]; };
+                for (int e = ew * 2; e < qn; e += 6) {  // warp-uniform: queue entries e, e + 1
+                    const bool two = e + 1 < qn;
+                    const uint32_t k1 = qkey(e), k2 = two ? qkey(e + 1) : k1;
+                    float x1, x2;
+                    coop2(k1, k2, x1, x2);
+                    if (lane == 0) {
+                        keep(k1, x1);
+                        if (two) keep(k2, x2);
                     }
                 }
                 tc::warp_arrive(&sm.qemp[b]);
@@ -680,7 +673,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                                          exact_step(0.f, x2.w, y2.w));
                     }
                     {
-                        float *ps = &sm.psq[E * 3 + ew][0][0];
+                        float *ps = sm.psq + (E * 3 + ew) * S::PSQW;
                         reinterpret_cast<float4 *>(ps)[lane] = p1;
                         reinterpret_cast<float4 *>(ps + 128)[lane] = p2;
                         __syncwarp();

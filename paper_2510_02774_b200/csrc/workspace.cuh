@@ -20,6 +20,8 @@ constexpr int PAIR_LIST = 64;
 constexpr int32_t CL_TRUNC = 1 << 30;
 constexpr int T3_META_REC = 1344;  // sizeof(T3Meta): 96 x (id, dv, norm: 4 B; pos: 1 B) + 12 x int2
 constexpr int CLREC = 4 + 2 * PAIR_LIST;
+constexpr int T3Q_CTAS = 256;    // tc3 global candidate overflow: CTAs (>= SMs) x 2 buffers
+constexpr int T3Q_GROUP = 4608;  // x entries (>= 96 * 95 / 2 pairs of a group)
 
 // small counters block (unsigned long long so atomicAdd works on it)
 enum Counter : int {
@@ -68,6 +70,10 @@ struct Workspace {
     // group of 96 slots -- pool ids, stored distances, row norms, positions, (vertex, k) per
     // pool -- fetched by ONE bulk copy (only carved when cap <= 96)
     unsigned char *s_meta;
+    // tc3 MULTI (D > 128): per CTA and queue buffer, the filter candidates beyond the
+    // shared-memory queue (a group has <= 96 * 95 / 2 pairs), so no group falls back to an
+    // exact sweep of all its pairs from global rows
+    uint32_t *t3q;
     int64_t n;
     int64_t msg_capacity;
 };
@@ -122,6 +128,7 @@ inline size_t carve(Workspace *w, void *base, int64_t n, int32_t cap, int64_t ms
     t.clcnt = (int32_t *)take(4 * N);
     const size_t SG = (cap > 0 && cap <= 96) ? N + 8 : 1;  // staging groups (<= one per pool + bins)
     t.s_meta = (unsigned char *)take((size_t)T3_META_REC * SG);
+    t.t3q = (uint32_t *)take((cap > 0 && cap <= 96) ? (size_t)4 * T3Q_CTAS * 2 * T3Q_GROUP : 4);
     t.n = n;
     t.msg_capacity = msg_capacity;
     if (w) *w = t;
