@@ -220,7 +220,8 @@ class _DevicePools:
     """The double-buffered pools of owned rows [lo, hi) plus round scratch, in HBM."""
 
     def __init__(self, data_dev: torch.Tensor, dim: int, cap: int, lo: int = 0, hi: int | None = None,
-                 n_total: int | None = None, msg_capacity: int | None = None, filtered: bool | None = None):
+                 n_total: int | None = None, msg_capacity: int | None = None, filtered: bool | None = None,
+                 in_place: bool = True):
         dev = data_dev.device
         self.dev = dev
         self.data = data_dev
@@ -239,9 +240,18 @@ class _DevicePools:
         self.read_ids = torch.empty((rows, cap), dtype=i32, device=dev)
         self.read_dists = torch.empty((rows, cap), dtype=f32, device=dev)
         self.read_count = torch.zeros(rows, dtype=i32, device=dev)
-        self.write_ids = torch.empty((rows, cap), dtype=i32, device=dev)
-        self.write_dists = torch.empty((rows, cap), dtype=f32, device=dev)
-        self.write_count = torch.zeros(rows, dtype=i32, device=dev)
+        # in place (default): ONE pool buffer.  A round's apply runs after its whole pair
+        # phase and rewrites only the pools that changed (incoming messages or tombstones),
+        # each from its own row -- the reference's cleared write buffer + swap, without the
+        # copy of every unchanged pool.  The double-buffered layout remains for states built
+        # with non-empty write buffers (the reference's manual-state tests).
+        self.in_place = bool(in_place)
+        if self.in_place:
+            self.write_ids, self.write_dists, self.write_count = self.read_ids, self.read_dists, self.read_count
+        else:
+            self.write_ids = torch.empty((rows, cap), dtype=i32, device=dev)
+            self.write_dists = torch.empty((rows, cap), dtype=f32, device=dev)
+            self.write_count = torch.zeros(rows, dtype=i32, device=dev)
         ws = int(_lib.lib.grnnd_workspace_bytes(rows, cap, self.msg_capacity))
         self.workspace = torch.zeros(ws, dtype=torch.uint8, device=dev)
         self.scratch_stats = torch.zeros(_lib.NSTATS, dtype=torch.int64, device=dev)
@@ -285,10 +295,11 @@ class _DevicePools:
         """clear_and_swap (builder.py:170-176): the written buffers become the read
         side; the old read side is logically cleared (count 0; slots beyond a row's
         count are never read)."""
-        self.read_ids, self.write_ids = self.write_ids, self.read_ids
-        self.read_dists, self.write_dists = self.write_dists, self.read_dists
-        self.read_count, self.write_count = self.write_count, self.read_count
-        self.write_count.zero_()
+        if not self.in_place:
+            self.read_ids, self.write_ids = self.write_ids, self.read_ids
+            self.read_dists, self.write_dists = self.write_dists, self.read_dists
+            self.read_count, self.write_count = self.write_count, self.read_count
+            self.write_count.zero_()
         self.version += 1
 
     # -- the four asynchronous steps --
@@ -376,11 +387,12 @@ class BuildState:
             n, cap = ri.shape
             dev = _device(device)
             with torch.cuda.device(dev):
-                pools = _DevicePools(upload(ds.data, dev), ds.dim, cap)
+                wc_given = write_count is not None and np.any(np.asarray(write_count) != 0)
+                pools = _DevicePools(upload(ds.data, dev), ds.dim, cap, in_place=not wc_given)
                 pools.read_ids.copy_(torch.from_numpy(ri))
                 pools.read_dists.copy_(torch.from_numpy(np.ascontiguousarray(read_dists, dtype=np.float32)))
                 pools.read_count.copy_(torch.from_numpy(np.ascontiguousarray(read_count, dtype=np.int32)))
-                if write_count is not None:
+                if wc_given:
                     wc = np.ascontiguousarray(write_count, dtype=np.int32)
                     pools.write_count.copy_(torch.from_numpy(wc))
                     if write_ids is not None:
@@ -417,9 +429,14 @@ class BuildState:
             self._snap_version = self.pools.version
         if side not in self._snap:
             P = self.pools
-            ids, dists, counts = ((P.read_ids, P.read_dists, P.read_count) if side == "read"
-                                  else (P.write_ids, P.write_dists, P.write_count))
-            out = self._masked(ids, dists, counts)
+            if side == "write" and P.in_place:  # logically cleared between rounds
+                n, cap = P.rows, P.cap
+                out = (np.full((n, cap), TOMBSTONE, np.int32), np.full((n, cap), np.inf, np.float32),
+                       np.zeros(n, np.int32))
+            else:
+                ids, dists, counts = ((P.read_ids, P.read_dists, P.read_count) if side == "read"
+                                      else (P.write_ids, P.write_dists, P.write_count))
+                out = self._masked(ids, dists, counts)
             for a in out:
                 a.setflags(write=False)
             self._snap[side] = out

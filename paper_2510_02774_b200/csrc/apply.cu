@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(256) apply_round_kernel(ApplyArgs a) {
     const int cap = a.cap;
     Outcome oc;
     unsigned long long own_total = 0;
-    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < a.n; t += warps) {
+    auto pool = [&](const int64_t t) {
         const int64_t tg = a.lo + t;
         const int64_t b = a.w.starts[t], e = a.w.starts[t + 1];
         // split point: messages from sources < tg come first (key = src * cap + j)
@@ -271,8 +271,39 @@ __global__ void __launch_bounds__(256) apply_round_kernel(ApplyArgs a) {
             }
         }
         apply_range<RPL>(P, a.w.i_id, a.w.i_dist, split, e, oc);
+        __syncwarp();  // in place: every lane's reads of the row precede the stores
         P.store(a.write_ids + t * cap, a.write_dists + t * cap);
-        if (lane == 0) a.write_count[t] = P.cnt;
+        if (lane == 0) {
+            a.write_count[t] = P.cnt;
+            if (a.in_place) a.w.dirty[t] = 0;
+        }
+    };
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (a.in_place) {
+        // one pool buffer: a pool without incoming messages and without tombstones is its
+        // own result (its entries re-inserted in slot order into an empty pool), so only the
+        // others are rewritten; the lanes screen 32 pools at a time and the clean pools'
+        // entries are counted as inserted survivors, as the reference counts them
+        for (int64_t t0 = wid * 32; t0 < a.n; t0 += warps * 32) {
+            const int64_t t = t0 + lane;
+            bool work = false;
+            unsigned long long kc = 0;
+            if (t < a.n) {
+                work = a.w.starts[t + 1] != a.w.starts[t] || a.w.dirty[t] != 0;
+                if (!work) kc = (unsigned long long)a.read_count[t];
+            }
+            kc = warp_sum(kc);
+            oc.ins += kc;
+            own_total += kc;
+            unsigned m = __ballot_sync(FULL, work);
+            while (m) {
+                const int l = __ffs(m) - 1;
+                m &= m - 1u;
+                pool(t0 + l);
+            }
+        }
+    } else {
+        for (int64_t t = wid; t < a.n; t += warps) pool(t);
     }
     if (lane == 0 && a.stats) {
         unsigned long long *st = (unsigned long long *)a.stats;

@@ -317,8 +317,10 @@ int grnnd_init_pools(const grnnd_pools *p, int32_t S_, uint64_t seed, int64_t *f
                                 S(s)));
     if (n > 0) {
         fill_i32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, S(s)>>>(p->read_count, n, S_);
-        fill_i32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, S(s)>>>(p->write_count, n, 0);
+        if (p->write_count != p->read_count)  // (in-place pools: one buffer)
+            fill_i32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, S(s)>>>(p->write_count, n, 0);
         GRNND_TRY(check_launch("fill_counts", 2));
+        GRNND_CUDA(cudaMemsetAsync(w.dirty, 0, (size_t)n, S(s)));
     }
     GRNND_CUDA(cudaMemsetAsync(w.ctr, 0, sizeof(unsigned long long) * C_NCOUNTERS, S(s)));
     return GRNND_OK;
@@ -378,6 +380,12 @@ static int apply_phase(const grnnd_pools *p, const Workspace &w, int32_t kind, c
     a.n = n;
     a.cap = p->cap;
     a.own_after_all = kind == 1 ? 1 : 0;
+    a.in_place = p->write_ids == p->read_ids ? 1 : 0;
+    if (a.in_place != (p->write_dists == p->read_dists ? 1 : 0) ||
+        a.in_place != (p->write_count == p->read_count ? 1 : 0)) {
+        set_error("write_ids / write_dists / write_count must all alias the read side or none of them");
+        return GRNND_EINVAL;
+    }
     a.w = w;
     a.stats = p->stats;
     GRNND_TRY(launch_apply_round(a, st));

@@ -386,6 +386,7 @@ __device__ __forceinline__ void decide_pool(const PropArgs &a, int k, int64_t v,
     __syncwarp();
     refp_total += refp;
     red_total += (unsigned long long)nm;
+    if (!a.slice_mode && nm > 0 && lane == 0) a.w.dirty[v] = 1;  // tombstoned: the apply must compact it
     unsigned long long base = 0;
     if (!a.slice_mode && nm > 0) {
         if (lane == 0) base = atomicAdd(&a.w.ctr[C_LIST], (unsigned long long)nm);

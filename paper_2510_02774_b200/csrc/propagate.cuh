@@ -83,6 +83,8 @@ struct ApplyArgs {
     int32_t cap;
     int32_t own_after_all;  // 0: own entries spliced at source == target (update round)
                             // 1: own entries after every inbox message (reverse round)
+    int32_t in_place;       // write_* == read_*: only pools with incoming messages or
+                            // tombstones (w.dirty) are rewritten; the rest are their own result
     Workspace w;
     int64_t *stats;
 };

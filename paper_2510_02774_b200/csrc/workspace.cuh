@@ -74,6 +74,7 @@ struct Workspace {
     // shared-memory queue (a group has <= 96 * 95 / 2 pairs), so no group falls back to an
     // exact sweep of all its pairs from global rows
     uint32_t *t3q;
+    uint8_t *dirty;      // [n] pool tombstoned this round (decide sets, the in-place apply clears)
     int64_t n;
     int64_t msg_capacity;
 };
@@ -129,6 +130,7 @@ inline size_t carve(Workspace *w, void *base, int64_t n, int32_t cap, int64_t ms
     const size_t SG = (cap > 0 && cap <= 96) ? N + 8 : 1;  // staging groups (<= one per pool + bins)
     t.s_meta = (unsigned char *)take((size_t)T3_META_REC * SG);
     t.t3q = (uint32_t *)take((cap > 0 && cap <= 96) ? (size_t)4 * T3Q_CTAS * 2 * T3Q_GROUP : 4);
+    t.dirty = (uint8_t *)take(N);
     t.n = n;
     t.msg_capacity = msg_capacity;
     if (w) *w = t;
