@@ -61,6 +61,8 @@ enum {
     GRNND_ST_OVERFLOWS = 11,  /* groups whose candidate queue overflowed into an exact sweep */
     GRNND_ST_REDIRECTABLE = 12, /* pairs meeting the redirect condition (instrumentation)      */
     GRNND_ST_RECPOOLS = 14,   /* pools with at least one redirect-capable pair (instrumentation) */
+    GRNND_ST_ACTIVE_K = 15,   /* pool entries whose pair phase ran (the rest: pools unchanged since a
+                                 round in which they had no redirect-capable pair -- a no-op) */
     GRNND_ST_LOST = 13,       /* messages a round could not hold (emit list beyond msg_capacity)
                                  or that reached the wrong rank: non-zero = the round is invalid,
                                  the Python layer raises DeviceError (GRNND_EWORKSPACE meaning) */

@@ -22,7 +22,7 @@ NSTATS = 20
 ST_MESSAGES, ST_REDIRECTS, ST_SURVIVORS, ST_REVERSE_ATTEMPTS = 0, 1, 2, 3
 ST_INSERTED, ST_DUPLICATE, ST_REPLACED, ST_REJECTED = 4, 5, 6, 7
 ST_PAIRS, ST_PAIRS_REF, ST_CANDIDATES, ST_OVERFLOWS = 8, 9, 10, 11
-ST_REDIRECTABLE, ST_LOST, ST_RECPOOLS = 12, 13, 14
+ST_REDIRECTABLE, ST_LOST, ST_RECPOOLS, ST_ACTIVE_K = 12, 13, 14, 15
 ST_TCV_CHECKED, ST_TCV_MAX_RATIO, ST_TCV_VIOLATIONS = 16, 17, 18
 MSG_WORDS = 5
 MAX_CAP = 256

@@ -90,6 +90,7 @@ class RoundStats:
     candidates: int = field(default=0, compare=False, repr=False)  # filter band re-evaluations
     redirectable: int = field(default=0, compare=False, repr=False)  # pairs meeting the redirect condition
     record_pools: int = field(default=0, compare=False, repr=False)  # pools with >= 1 such pair
+    active_entries: int = field(default=0, compare=False, repr=False)  # entries whose pair phase ran
 
     @classmethod
     def from_counters(cls, kind: str, c) -> "RoundStats":
@@ -112,6 +113,7 @@ class RoundStats:
             candidates=c[_lib.ST_CANDIDATES],
             redirectable=c[_lib.ST_REDIRECTABLE],
             record_pools=c[_lib.ST_RECPOOLS],
+            active_entries=c[_lib.ST_ACTIVE_K],
         )
         if kind == "update":
             st.survivors = st.messages - st.redirects

@@ -291,6 +291,12 @@ __global__ void __launch_bounds__(256) apply_round_kernel(ApplyArgs a) {
             if (t < a.n) {
                 work = a.w.starts[t + 1] != a.w.starts[t] || a.w.dirty[t] != 0;
                 if (!work) kc = (unsigned long long)a.read_count[t];
+                // next update round's pair phase: only pools that changed, or whose pair phase
+                // found a redirect-capable pair (dirty).  After an update round an unchanged,
+                // clean pool ran a pair phase that found none (or was idle already); a reverse
+                // round runs no pair phase, so it can only wake pools up
+                if (work) a.w.idle[t] = 0;
+                else if (!a.own_after_all) a.w.idle[t] = 1;
             }
             kc = warp_sum(kc);
             oc.ins += kc;
@@ -303,7 +309,10 @@ __global__ void __launch_bounds__(256) apply_round_kernel(ApplyArgs a) {
             }
         }
     } else {
-        for (int64_t t = wid; t < a.n; t += warps) pool(t);
+        for (int64_t t = wid; t < a.n; t += warps) {
+            pool(t);
+            if (lane == 0) a.w.idle[t] = 0;  // (two buffers: every pool rewritten)
+        }
     }
     if (lane == 0 && a.stats) {
         unsigned long long *st = (unsigned long long *)a.stats;

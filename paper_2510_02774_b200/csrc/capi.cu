@@ -321,6 +321,7 @@ int grnnd_init_pools(const grnnd_pools *p, int32_t S_, uint64_t seed, int64_t *f
             fill_i32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, S(s)>>>(p->write_count, n, 0);
         GRNND_TRY(check_launch("fill_counts", 2));
         GRNND_CUDA(cudaMemsetAsync(w.dirty, 0, (size_t)n, S(s)));
+        GRNND_CUDA(cudaMemsetAsync(w.idle, 0, (size_t)n, S(s)));
     }
     GRNND_CUDA(cudaMemsetAsync(w.ctr, 0, sizeof(unsigned long long) * C_NCOUNTERS, S(s)));
     return GRNND_OK;

@@ -61,16 +61,22 @@ __global__ void bin_kernel(const int32_t *__restrict__ read_count, int64_t n, in
     // instructions per vertex) are computed warp-cooperatively for the warp's 32 vertices,
     // so a warp costs sum(ceil(k / 32)) hash rounds instead of max(k); each lane then runs
     // its own vertex's (cheap) swap chain from the staged swap targets.
-    __shared__ unsigned long long s_sum;
+    __shared__ unsigned long long s_sum, s_act;
     extern __shared__ uint8_t fy_scratch[];  // [blockDim.x][cap] perm + [blockDim.x][cap] swap targets
-    if (threadIdx.x == 0) s_sum = 0;
+    if (threadIdx.x == 0) s_sum = s_act = 0;
     __syncthreads();
     const int lane = lane_id();
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int k = 0, b = 0;
+    unsigned long long ak = 0;
     if (v < n) {
         k = read_count[v];
         b = bin_of(k, tc_bins);
+        // Round API: a pool unchanged since a round in which it had no redirect-capable pair
+        // still has none -- the condition d(a, b) < max(dv_a, dv_b) does not depend on the
+        // visiting order -- so its pair phase would emit nothing and tombstone nothing: skip
+        if (!slice_mode && w.idle[v]) b = 0;
+        if (b > 0) ak = (unsigned long long)k;
         if (b > 0) {
             const unsigned peers = __match_any_sync(__activemask(), b);
             const int leader = __ffs(peers) - 1;
@@ -123,9 +129,12 @@ __global__ void bin_kernel(const int32_t *__restrict__ read_count, int64_t n, in
     }
     unsigned long long ks = (unsigned long long)k;
     ks = warp_sum(ks);
+    ak = warp_sum(ak);
     if (lane == 0 && ks) atomicAdd(&s_sum, ks);
+    if (lane == 0 && ak) atomicAdd(&s_act, ak);
     __syncthreads();
     if (threadIdx.x == 0 && s_sum && stats) atomicAdd((unsigned long long *)&stats[GRNND_ST_MESSAGES], s_sum);
+    if (threadIdx.x == 0 && s_act && stats) atomicAdd((unsigned long long *)&stats[GRNND_ST_ACTIVE_K], s_act);
 }
 
 // ---------------------------------------------------------------------------------

@@ -75,6 +75,9 @@ struct Workspace {
     // exact sweep of all its pairs from global rows
     uint32_t *t3q;
     uint8_t *dirty;      // [n] pool tombstoned this round (decide sets, the in-place apply clears)
+    uint8_t *idle;       // [n] 1: the pool's pair phase is a no-op this round (unchanged since a
+                         // round in which it had no redirect-capable pair); set by the apply,
+                         // zero (all run) in a fresh workspace and after init
     int64_t n;
     int64_t msg_capacity;
 };
@@ -131,6 +134,7 @@ inline size_t carve(Workspace *w, void *base, int64_t n, int32_t cap, int64_t ms
     t.s_meta = (unsigned char *)take((size_t)T3_META_REC * SG);
     t.t3q = (uint32_t *)take((cap > 0 && cap <= 96) ? (size_t)4 * T3Q_CTAS * 2 * T3Q_GROUP : 4);
     t.dirty = (uint8_t *)take(N);
+    t.idle = (uint8_t *)take(N);
     t.n = n;
     t.msg_capacity = msg_capacity;
     if (w) *w = t;
