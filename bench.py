@@ -49,7 +49,7 @@ CONFIGS = {
     "c3": (1_000_000, 960, "l2", "GIST1M-shape synthetic 1M×960 fp32 L2, R=96 (high-dim, distance-gather bound)"),
     "c4": (10_000_000, 96, "ip", "Deep10M-shape synthetic 10M×96 fp32 inner-product (L2-normalised rows)"),
 }
-NCU_FILE = ROOT / "profiles" / "r2_pair_phase_ncu.json"
+NCU_FILE = ROOT / "profiles" / "r2_pair_phase_ncu.json"  # tools/gpu_round.sh FULL=1
 LS = (32, 64, 96, 128, 256)
 
 
@@ -349,8 +349,14 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     pk, pk_kind = peaks()
     D = args.dim
     sum_k = [s.messages for s in upd]
-    alg_bytes = [(4 * D + 40) * k for k in sum_k]  # SURVEY 8(d) d3 per update round
+    # SURVEY 8(d) d3 per update round over the pool entries the pair phase processed (pools
+    # unchanged since a pair phase without redirect-capable pairs are skipped: their pair
+    # phase is a no-op), and the reference-equivalent figure over every live entry
+    act_k = [s.active_entries for s in upd]
+    alg_bytes = [(4 * D + 40) * k for k in act_k]
+    ref_bytes = [(4 * D + 40) * k for k in sum_k]
     ach_gbs = sum(alg_bytes) / (sum(prop_ms) * 1e-3) / 1e9
+    ref_gbs = sum(ref_bytes) / (sum(prop_ms) * 1e-3) / 1e9
     pairs_ref = [s.pairs_ref for s in upd]
     pairs_all = [s.pairs for s in upd]
     cands = [s.candidates for s in upd]
@@ -396,6 +402,12 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
                          "peak_source": pk_kind,
                          "alg_bytes_per_round": int(sum(alg_bytes) / len(alg_bytes)),
                          "ms_per_round": round(sum(prop_ms) / len(prop_ms), 3),
+                         "processed_entry_frac": round(sum(act_k) / max(sum(sum_k), 1), 4),
+                         "reference_equivalent": {
+                             "alg_bytes_per_round": int(sum(ref_bytes) / len(ref_bytes)),
+                             "gbs": round(ref_gbs, 1),
+                             "note": "(4D+40) x every live pool entry per update round (the reference's "
+                                     "pair-phase work, SURVEY 8(d) d3) over the same time"},
                          "compute_term": {"flops_per_round": int(sum(flops) / len(flops)),
                                           "tflops_achieved": round(sum(flops) / (sum(prop_ms) * 1e-3) / 1e12, 2),
                                           "fp32_peak_tflops": round(fp32_tflops, 1),
