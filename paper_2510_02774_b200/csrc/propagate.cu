@@ -468,16 +468,31 @@ __global__ void __launch_bounds__(dec_warps<MW>() * 32, 4) decide_kernel(PropArg
     uint8_t *pos = sm.pos[wib];
     unsigned long long red_total = 0, refp_total = 0, recpools = 0;
 
-    for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
+    // Round API: the lanes screen 32 vertices at a time; only pools with a redirect-capable
+    // pair have anything to decide (the others emit and tombstone nothing -- their survivors
+    // stay in the row -- and the reference visits every one of their pairs)
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t step = a.slice_mode ? warps : warps * 32;
+    for (int64_t v0 = a.slice_mode ? wid : wid * 32; v0 < n; v0 += step) {
+        unsigned todo = 1u;  // slice mode: this warp's one vertex v0
+        if (!a.slice_mode) {
+            const int64_t vl = v0 + lane;
+            int kl = 0;
+            int32_t cl = 0;
+            if (vl < n) {
+                kl = a.read_count[vl];
+                cl = kl >= 2 ? a.w.clcnt[vl] : 0;
+            }
+            unsigned long long rp = (kl >= 2 && cl == 0) ? (unsigned long long)kl * (unsigned long long)(kl - 1) / 2ull : 0ull;
+            refp_total += warp_sum(rp) * (lane == 0 ? 1ull : 0ull);
+            todo = __ballot_sync(FULL, cl != 0);
+        }
+        while (todo) {
+        const int64_t v = v0 + (__ffs(todo) - 1);
+        todo &= todo - 1u;
         const int k = a.read_count[v];
         if (k < 2) continue;  // no pairs (slice-mode survivors of k <= 1 come from bin_kernel)
         const int32_t clc = a.w.clcnt[v];
-        if (!a.slice_mode && clc == 0) {
-            // no redirect-capable pair: nothing is emitted or tombstoned (survivors stay in the
-            // row, which the round API keeps packed), and the reference visits every pair
-            if (lane == 0) refp_total += (unsigned long long)k * (unsigned long long)(k - 1) / 2ull;
-            continue;
-        }
         recpools += clc != 0 ? 1ull : 0ull;
         for (int s = lane; s < k; s += 32) {
             ids[s] = a.read_ids[v * cap + s];
@@ -549,6 +564,7 @@ __global__ void __launch_bounds__(dec_warps<MW>() * 32, 4) decide_kernel(PropArg
         };
         decide_pool<MW>(a, k, v, ids, pos, sm.perm[wib], sm.e_tgt[wib], sm.e_id[wib], sm.e_key[wib], masks, dist_of,
                         red_total, refp_total);
+        }
     }
     refp_total = warp_sum(refp_total);
     if (lane == 0 && a.stats) {
