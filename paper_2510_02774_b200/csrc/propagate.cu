@@ -253,6 +253,7 @@ __device__ __forceinline__ void tile_dot(float (&acc)[T * T], const float4 *__re
 }
 
 #include "pairs.cuh"
+#include "lazy.cuh"
 
 // ---------------------------------------------------------------------------------
 // 3. decide kernel: anchor-serial rule over the masks, emission, tombstones
@@ -485,7 +486,7 @@ __global__ void __launch_bounds__(dec_warps<MW>() * 32, 4) decide_kernel(PropArg
             }
             unsigned long long rp = (kl >= 2 && cl == 0) ? (unsigned long long)kl * (unsigned long long)(kl - 1) / 2ull : 0ull;
             refp_total += warp_sum(rp) * (lane == 0 ? 1ull : 0ull);
-            todo = __ballot_sync(FULL, cl != 0);
+            todo = __ballot_sync(FULL, cl != 0 && cl != CL_DONE);
         }
         while (todo) {
         const int64_t v = v0 + (__ffs(todo) - 1);
@@ -681,6 +682,9 @@ static int launch_tc3_pairs(const PropArgs &a, int bin, cudaStream_t st) {
 #ifndef GRNND_TC
 #define GRNND_TC 1  // tensor-core Gram pre-screen (tc_pairs.cuh) for D <= 128, R <= 128
 #endif
+#ifndef GRNND_NO_LAZY
+#define GRNND_NO_LAZY 0  // 1: the exact CUDA-core kernel for k <= 32 too (A/B builds)
+#endif
 #ifndef GRNND_TC_MULTI
 #define GRNND_TC_MULTI 1  // ... and for D > 128 with R <= 96 (tc3 MULTI)
 #endif
@@ -721,13 +725,25 @@ int launch_propagate(const PropArgs &a, cudaStream_t st) {
         if (a.cap > 16) GRNND_TRY(launch_tc_pairs<32>(a, 2, st));
         if (a.cap > 1) GRNND_TRY(launch_tc_pairs<16>(a, 1, st));
     } else {
+    // k <= 32, D <= 128, round API: the anchor-serial lazy kernel evaluates only the pairs the
+    // reference evaluates (first rounds of a build) and decides the pools itself
+    const bool lazy = !a.slice_mode && a.order_code == 0 && a.dim <= 128 && !GRNND_NO_LAZY;
+    if (lazy) {
+        const size_t smem = sizeof(LazyWarp) * LZ_WARPS;
+        static SmemOptIn optin;
+        GRNND_CUDA(optin.ensure(lazy_pairs_kernel, smem));
+        int per_sm = 0;
+        GRNND_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lazy_pairs_kernel, LZ_WARPS * 32, smem));
+        lazy_pairs_kernel<<<device_sm_count() * (per_sm > 0 ? per_sm : 1), LZ_WARPS * 32, smem, st>>>(a);
+        GRNND_TRY(check_launch("lazy_pairs_kernel"));
+    }
     // k in (64, 96] with R <= 96 (the benchmark shape): a slab sized for 96 rows fits four
     // CTAs per SM where the 128-row one fits three
     if (a.cap > 64 && a.cap <= 96) GRNND_TRY((launch_pairs<96, 1, 128, 3, 4>(a, 4, st)));
     if (a.cap > 96) GRNND_TRY((launch_pairs<128, 1, 128, 3, 4>(a, 4, st)));
     if (a.cap > 32) GRNND_TRY((launch_pairs<64, 1, 128, 3, 2>(a, 3, st)));
-    if (a.cap > 16) GRNND_TRY((launch_pairs<32, GRNND_B2_BATCH, 128, 3, 2>(a, 2, st)));
-    if (a.cap > 1) GRNND_TRY((launch_pairs<16, GRNND_B1_BATCH, 128, 2, 2>(a, 1, st)));
+    if (a.cap > 16 && !lazy) GRNND_TRY((launch_pairs<32, GRNND_B2_BATCH, 128, 3, 2>(a, 2, st)));
+    if (a.cap > 1 && !lazy) GRNND_TRY((launch_pairs<16, GRNND_B1_BATCH, 128, 2, 2>(a, 1, st)));
     }
     auto dec = [&](auto kern, int warps) {
         const int64_t blocks = std::min<int64_t>((n + warps - 1) / warps, (int64_t)device_sm_count() * 16);

@@ -18,6 +18,7 @@ constexpr int HEAVY_SEG = 32;  // segments longer than this are sorted by a CTA
 // distances the list lacks.  (16-byte aligned records: bulk-stored by tc3.)
 constexpr int PAIR_LIST = 64;
 constexpr int32_t CL_TRUNC = 1 << 30;
+constexpr int32_t CL_DONE = 1 << 29;  // clcnt: the pool was decided by its pair kernel (lazy.cuh)
 constexpr int T3_META_REC = 1344;  // sizeof(T3Meta): 96 x (id, dv, norm: 4 B; pos: 1 B) + 12 x int2
 constexpr int CLREC = 4 + 2 * PAIR_LIST;
 constexpr int T3Q_CTAS = 256;    // tc3 global candidate overflow: CTAs (>= SMs) x 2 buffers
