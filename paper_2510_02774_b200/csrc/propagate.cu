@@ -682,8 +682,8 @@ static int launch_tc3_pairs(const PropArgs &a, int bin, cudaStream_t st) {
 #ifndef GRNND_TC
 #define GRNND_TC 1  // tensor-core Gram pre-screen (tc_pairs.cuh) for D <= 128, R <= 128
 #endif
-#ifndef GRNND_NO_LAZY
-#define GRNND_NO_LAZY 0  // 1: the exact CUDA-core kernel for k <= 32 too (A/B builds)
+#ifndef GRNND_LAZY_ROUNDS
+#define GRNND_LAZY_ROUNDS 2  // update rounds (stream ids 1..) whose k <= 32 pools run lazy_pairs_kernel
 #endif
 #ifndef GRNND_TC_MULTI
 #define GRNND_TC_MULTI 1  // ... and for D > 128 with R <= 96 (tc3 MULTI)
@@ -727,7 +727,9 @@ int launch_propagate(const PropArgs &a, cudaStream_t st) {
     } else {
     // k <= 32, D <= 128, round API: the anchor-serial lazy kernel evaluates only the pairs the
     // reference evaluates (first rounds of a build) and decides the pools itself
-    const bool lazy = !a.slice_mode && a.order_code == 0 && a.dim <= 128 && !GRNND_NO_LAZY;
+    // (rounds 1-2: redirect-dense random pools, 17-19% of the pairs evaluated; by round 3 the
+    // all-pairs tile kernel plus decide is as fast)
+    const bool lazy = !a.slice_mode && a.order_code == 0 && a.dim <= 128 && a.stream_id <= GRNND_LAZY_ROUNDS;
     if (lazy) {
         const size_t smem = sizeof(LazyWarp) * LZ_WARPS;
         static SmemOptIn optin;
