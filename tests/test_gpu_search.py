@@ -159,3 +159,25 @@ def test_c2_back_to_back_builds_equal_reference_digest(g, golden):
         e = int(o[-1])
         assert hashlib.sha256(o.astype(np.int64).tobytes()).hexdigest() == meta["sha256_offsets"]
         assert hashlib.sha256(nb[:e].cpu().numpy().astype(np.int32).tobytes()).hexdigest() == meta["sha256_neighbor_ids"]
+
+
+def test_c4_ip_build_equals_oracle_digest(g):
+    """C4 (10M x 96, inner product over L2-normalised rows) on one B200: the graph digest
+    equals the CPU oracle's build of the same workload (profiles/oracle_digest_c4.json,
+    tests/golden/make_oracle_digest.py; the oracle equals the reference's digests at C1-C3)."""
+    from pathlib import Path
+
+    from paper_2510_02774_b200.builder import DeviceBuild, upload
+
+    if torch.cuda.get_device_properties(0).total_memory < 150e9:
+        pytest.skip("needs a 180 GB B200")
+    od = json.loads((Path(__file__).resolve().parents[1] / "profiles" / "oracle_digest_c4.json").read_text())
+    data = np.random.default_rng(1).standard_normal((10_000_000, 96), dtype=np.float32)
+    eng = DeviceBuild(upload(data, torch.device("cuda")), 96, g.BuildParams(S=20, R=96, T1=4, T2=15, rho=0.6, seed=1),
+                      metric="ip")
+    off, nb, bad, fail = eng.run()
+    o = off.cpu().numpy()
+    e = int(o[-1])
+    assert e == od["edges"]
+    assert sha(o.astype(np.int64)) == od["sha256_offsets"]
+    assert sha(nb[:e].cpu().numpy().astype(np.int32)) == od["sha256_neighbor_ids"]
