@@ -48,7 +48,11 @@ CONFIGS = {
     "c2": (1_000_000, 128, "l2", "SIFT1M-shape synthetic 1M×128 fp32 L2, R=96, single B200"),
     "c3": (1_000_000, 960, "l2", "GIST1M-shape synthetic 1M×960 fp32 L2, R=96 (high-dim, distance-gather bound)"),
     "c4": (10_000_000, 96, "ip", "Deep10M-shape synthetic 10M×96 fp32 inner-product (L2-normalised rows)"),
+    # the realistic-recall regime -- clustered(5) with queries held out of the
+    # same draw (a second seed would move the cluster centres, io.py:151-153)
+    "c2c": (1_000_000, 128, "l2", "synthetic clustered(5) 1M×128 fp32 L2 with 1000 held-out queries, R=96"),
 }
+HELD_OUT = {"c2c"}  # configs whose data is generate(n + 1000, D, "clustered", seed=1)
 NCU_FILE = ROOT / "profiles" / "r2_pair_phase_ncu.json"  # tools/gpu_round.sh FULL=1
 LS = (32, 64, 96, 128, 256)
 
@@ -68,6 +72,7 @@ def parse():
     n, d, metric, wl = CONFIGS[a.config]
     a.metric_kind = metric
     a.workload = wl
+    a.clustered = a.config in HELD_OUT
     if a.n is not None or a.dim is not None:
         n, d = a.n or n, a.dim or d
         a.workload = f"synthetic gaussian {n}x{d} fp32 {metric.upper()}, S=20 R=96 T1=4 T2=15"
@@ -83,9 +88,19 @@ def config_of(args) -> dict:
                   else "vectors fit in L2 (no flush)"}
 
 
-def make_data(n: int, dim: int) -> np.ndarray:
-    """generate(n, dim, "gaussian", seed=1) (io.py:131-156), with numpy directly."""
-    return np.random.default_rng(1).standard_normal((n, dim), dtype=np.float32)
+def make_data(n: int, dim: int, clustered: bool = False) -> np.ndarray:
+    """generate(n, dim, "gaussian", seed=1) (io.py:131-156), with numpy directly; clustered:
+    the first n rows of generate(n + 1000, dim, "clustered", seed=1, clusters=5)."""
+    if not clustered:
+        return np.random.default_rng(1).standard_normal((n, dim), dtype=np.float32)
+    return held_out_draw(n, dim)[:n]
+
+
+def held_out_draw(n: int, dim: int) -> np.ndarray:
+    g = np.random.default_rng(1)
+    centres = 10.0 * g.standard_normal((5, dim))
+    which = g.integers(0, 5, size=n + 1000)
+    return (centres[which] + g.standard_normal((n + 1000, dim))).astype(np.float32)
 
 
 def peaks():
@@ -172,7 +187,7 @@ def run_reference(args, rank: int):
     minutes (a C2 build takes ~90 s on 16 threads) and the line reports what ran."""
     if rank != 0:
         return
-    data = make_data(args.n, args.dim)
+    data = make_data(args.n, args.dim, args.clustered)
     steps = max(1, min(args.steps, int(os.environ.get("GRNND_REF_MAX_STEPS", "1"))))
     vals, threads, edges = [], 0, 0
     for _ in range(steps):
@@ -208,12 +223,14 @@ def parity_leg(args, g, data_dev, offsets, nbrs, edges):
     out = {"sha256_offsets": hashlib.sha256(off_h.astype(np.int64).tobytes()).hexdigest(),
            "sha256_neighbor_ids": hashlib.sha256(nb_h.astype(np.int32).tobytes()).hexdigest()}
     ref = None
-    for name, (n, d, metric, _) in CONFIGS.items():
-        f = ROOT / "tests" / "golden" / f"{name}_reference.npz"
-        if n == args.n and d == args.dim and metric == args.metric_kind and f.exists():
-            ref = np.load(f)
+    f = ROOT / "tests" / "golden" / f"{args.config}_reference.npz"
+    if args.config in CONFIGS and CONFIGS[args.config][:2] == (args.n, args.dim) and f.exists():
+        ref = np.load(f)
     dev = data_dev.device
-    q = np.random.default_rng(2).standard_normal((1000, args.dim), dtype=np.float32)  # generate(1000, D, seed=2)
+    if args.clustered:  # the held-out rows of the same draw
+        q = np.ascontiguousarray(held_out_draw(args.n, args.dim)[args.n:])
+    else:
+        q = np.random.default_rng(2).standard_normal((1000, args.dim), dtype=np.float32)  # generate(1000, D, seed=2)
     if args.metric_kind == "ip":
         q = q / np.sqrt((q.astype(np.float64) ** 2).sum(1, keepdims=True)).astype(np.float32)
     from paper_2510_02774_b200.builder import upload
@@ -245,10 +262,9 @@ def parity_leg(args, g, data_dev, offsets, nbrs, edges):
         # build (tests/golden/make_oracle_digest.py), the restatement pinned to the reference's
         # own builds at C1-C3
         od = None
-        for name, (n, d, metric, _) in CONFIGS.items():
-            f = ROOT / "profiles" / f"oracle_digest_{name}.json"
-            if n == args.n and d == args.dim and metric == args.metric_kind and f.exists():
-                od = json.loads(f.read_text())
+        f = ROOT / "profiles" / f"oracle_digest_{args.config}.json"
+        if args.config in CONFIGS and CONFIGS[args.config][:2] == (args.n, args.dim) and f.exists():
+            od = json.loads(f.read_text())
         if od is not None and "sha256_offsets" in od:
             out["digest_match"] = (out["sha256_offsets"] == od["sha256_offsets"]
                                    and out["sha256_neighbor_ids"] == od["sha256_neighbor_ids"])
@@ -288,7 +304,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
         return float(t.item())
 
     ip = args.metric_kind == "ip"
-    data = make_data(args.n, args.dim)
+    data = make_data(args.n, args.dim, args.clustered)
     params = g.BuildParams(**PARAMS)
     data_dev = upload(data, dev)
     if world > 1:
@@ -346,9 +362,10 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     else:
         def api_build(d, p):
             return g.build(d, p, metric=args.metric_kind)
-    api_build(pinned_ds, params)  # warm the allocator for this path
+    graph = api_build(pinned_ds, params)  # warm the device and pinned-host allocators for this path
     e2e = []
     for _ in range(args.steps):
+        del graph  # a caller keeps one graph at a time: its host blocks are reused
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
