@@ -41,7 +41,9 @@ CONFIGS = {
     "c1": (20_000, 128),
     "c2": (1_000_000, 128),
     "c3": (1_000_000, 960),
+    "c2c": (1_000_000, 128),  # clustered(5), queries held out of the same draw
 }
+HELD_OUT = {"c2c"}
 LS = (32, 64, 96, 128, 256)
 NQ = 1000
 NS = 1000  # sampled vertices for k-NN-graph recall
@@ -75,7 +77,15 @@ def main() -> None:
     grnnd.build(grnnd.generate(2000, d, "gaussian", seed=3),
                 BuildParams(S=20, R=96, T1=2, T2=2, rho=0.6, seed=1, workers=threads))
 
-    ds = grnnd.generate(n, d, "gaussian", seed=1)
+    if name in HELD_OUT:
+        # one draw of n + NQ rows (a different seed would move the cluster centres, io.py:151-153);
+        # the last NQ rows are the queries
+        full = grnnd.generate(n + NQ, d, "clustered", seed=1).data
+        ds = grnnd.Dataset(np.ascontiguousarray(full[:n]))
+        held = np.ascontiguousarray(full[n:])
+    else:
+        ds = grnnd.generate(n, d, "gaussian", seed=1)
+        held = None
     params = BuildParams(S=20, R=96, T1=4, T2=15, rho=0.6, seed=1, workers=threads)
     stats: list = []
     t0 = time.perf_counter()
@@ -87,7 +97,7 @@ def main() -> None:
     stats_arr = np.array([[getattr(s, f) for f in fields] for s in stats], np.int64)
     np.savez(f"/tmp/{name}_ref_graph.npz", offsets=g.offsets, neighbor_ids=g.neighbor_ids)
 
-    q = grnnd.generate(NQ, d, "gaussian", seed=2).data
+    q = held if held is not None else grnnd.generate(NQ, d, "gaussian", seed=2).data
     t0 = time.perf_counter()
     truth = brute_force_knn_batch(ds, q, 10, threads=threads)
     bf_s = time.perf_counter() - t0
@@ -103,7 +113,9 @@ def main() -> None:
     print(f"knn-graph recall@10 {kg:.4f}", flush=True)
 
     out = Path(__file__).resolve().parent / f"{name}_reference.npz"
-    meta = {"n": n, "dim": d, "S": 20, "R": 96, "T1": 4, "T2": 15, "rho": 0.6, "seed": 1,
+    meta = {"n": n, "dim": d, "distribution": "clustered" if name in HELD_OUT else "gaussian",
+            "queries": "held out (last 1000 rows of one draw)" if name in HELD_OUT else "generate(1000, D, seed=2)",
+            "S": 20, "R": 96, "T1": 4, "T2": 15, "rho": 0.6, "seed": 1,
             "threads": threads, "build_seconds": build_s, "brute_force_seconds": bf_s,
             "numba": __import__("numba").__version__, "edges": int(g.offsets[-1]),
             "sha256_offsets": sha(g.offsets.astype(np.int64)),
