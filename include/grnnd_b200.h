@@ -179,6 +179,14 @@ typedef struct {
 int grnnd_row_norms(const float *data, int64_t n, int32_t dim, int32_t ld, float *out,
                     grnnd_stream_t s);
 
+/* Width of the tensor-core filter's error band relative to the pools' distances: out
+ * (device double[2]) = (sum over every read entry of |member|^2 / its stored distance,
+ * number of entries).
+ * The band is 2^-8 (|a|^2 + |b|^2) wide, so data far from the origin relative to its
+ * neighbour distances (clustered, all-positive descriptors) makes most pairs candidates; the
+ * host then keeps the exact pair phase (the graph is the same either way). */
+int grnnd_band_terms(const grnnd_pools *p, double *out, grnnd_stream_t s);
+
 /* builder.init_neighbors (:221-257): sample S ids, their distances, count = S.
  * fail_flag: device int64[1]. */
 int grnnd_init_pools(const grnnd_pools *p, int32_t S, uint64_t seed, int64_t *fail_flag,

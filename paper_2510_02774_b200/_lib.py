@@ -93,6 +93,7 @@ _SIGS = {
     "grnnd_finalize_pools": (C.c_int, [C.POINTER(Pools), _vp, _vp, _vp, _vp]),
     "grnnd_check_finite": (C.c_int, [_vp, _i64, _i32, _i32, _vp, _vp]),
     "grnnd_row_norms": (C.c_int, [_vp, _i64, _i32, _i32, _vp, _vp]),
+    "grnnd_band_terms": (C.c_int, [C.POINTER(Pools), _vp, _vp]),
     "grnnd_brute_force_workspace_bytes": (_sz, [_i64, _i64, _i32]),
     "grnnd_brute_force": (C.c_int, [_vp, _i64, _i32, _i32, _vp, _i64, _i32, _vp, _vp, _vp, _sz, _vp]),
     "grnnd_search_visited_bytes": (_sz, [_i64, _i64]),

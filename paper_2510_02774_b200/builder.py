@@ -263,6 +263,8 @@ class _DevicePools:
         if filtered is None:
             filtered = os.environ.get("GRNND_EXACT_PAIRS", "0") != "1"
         self.norms = None
+        self._filter_ok = None
+        self.band_ratio = None
         if filtered:
             self.norms = torch.empty(self.n_total, dtype=f32, device=dev)
             self.compute_norms()
@@ -285,13 +287,29 @@ class _DevicePools:
             norms.data_ptr() if norms is not None else None,
         )
 
-    @staticmethod
-    def filtered_round(stream_id: int) -> bool:
+    BAND_LIMIT = 0.05  # filter band / mean stored distance above which the filter is not used
+
+    def filtered_round(self, stream_id: int) -> bool:
         """Pair-phase mode of an update round.  The first rounds start from random pools,
         where most pairs meet the redirect condition (68% / 32% / 17% of all pairs in rounds
         1-3 at C2) and the tensor-core filter settles few of them: those rounds run the
-        exact-only pair phase; later rounds the filtered one.  Same graph either way."""
-        return stream_id > int(os.environ.get("GRNND_EXACT_FIRST_ROUNDS", EXACT_FIRST_ROUNDS))
+        exact-only pair phase; later rounds the filtered one -- unless the filter's error band
+        (2^-8 (|a|^2 + |b|^2)) is wide against the pools' distances, i.e. the
+        data lie far from the origin relative to their neighbour distances (clustered data:
+        85% of pairs would be candidates).  That is measured once, at the first filtered
+        round (one host read per build).  Same graph either way."""
+        if stream_id <= int(os.environ.get("GRNND_EXACT_FIRST_ROUNDS", EXACT_FIRST_ROUNDS)):
+            return False
+        if self.norms is None or os.environ.get("GRNND_FORCE_FILTER") == "1":
+            return self.norms is not None
+        if self._filter_ok is None:
+            out = torch.zeros(2, dtype=torch.float64, device=self.dev)
+            with torch.cuda.device(self.dev):
+                _lib.call("grnnd_band_terms", C.byref(self.struct()), out.data_ptr(), _stream(self.dev))
+            sr, cnt = (float(x) for x in out.cpu())
+            self.band_ratio = 2.0 ** -7 * sr / max(cnt, 1.0)  # mean band / stored distance
+            self._filter_ok = self.band_ratio <= self.BAND_LIMIT
+        return self._filter_ok
 
     def swap(self) -> None:
         """clear_and_swap (builder.py:170-176): the written buffers become the read
@@ -311,6 +329,7 @@ class _DevicePools:
         p = self.struct()
         _lib.call("grnnd_init_pools", C.byref(p), S, seed & MASK64, fail.data_ptr(), _stream(self.dev))
         self.version += 1
+        self._filter_ok = None  # re-measured by the next build's first filtered round
         return fail
 
     @_on_device

@@ -512,6 +512,43 @@ int grnnd_sorted_rows(const int32_t *ids, const float *dists, const int32_t *cou
 }
 
 
+__global__ void band_terms_kernel(const int32_t *__restrict__ ids, const float *__restrict__ dists,
+                                  const int32_t *__restrict__ counts, const float *__restrict__ norms, int64_t n,
+                                  int32_t cap, double *out) {
+    double sn = 0.0, sd = 0.0;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * cap; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = e / cap;
+        const int s = (int)(e - v * cap);
+        if (s < counts[v]) {
+            const int32_t id = ids[e];
+            if (id >= 0) {  // |member|^2 / its stored distance, averaged over the entries
+                const double dv = (double)dists[e];
+                sn += (double)norms[id] / (dv > 1e-30 ? dv : 1e-30);
+                sd += 1.0;
+            }
+        }
+    }
+    sn = warp_sum(sn);
+    sd = warp_sum(sd);
+    if (lane_id() == 0) {
+        atomicAdd(&out[0], sn);
+        atomicAdd(&out[1], sd);
+    }
+}
+
+int grnnd_band_terms(const grnnd_pools *p, double *out, grnnd_stream_t s) {
+    if (!p || !out || !p->norms) {
+        set_error("band_terms: pools with norms and an output buffer required");
+        return GRNND_EINVAL;
+    }
+    const int64_t n = p->hi - p->lo;
+    GRNND_CUDA(cudaMemsetAsync(out, 0, 2 * sizeof(double), S(s)));
+    if (n <= 0) return GRNND_OK;
+    band_terms_kernel<<<(unsigned)(device_sm_count() * 8), 256, 0, S(s)>>>(p->read_ids, p->read_dists, p->read_count,
+                                                                          p->norms, n, p->cap, out);
+    return check_launch("band_terms_kernel");
+}
+
 int grnnd_row_norms(const float *data, int64_t n, int32_t dim, int32_t ld, float *out, grnnd_stream_t s) {
     if (dim < 1 || ld < dim || n < 0) {
         set_error("row_norms: bad n/dim/ld");

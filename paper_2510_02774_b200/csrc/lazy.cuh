@@ -136,8 +136,7 @@ __global__ void __launch_bounds__(LZ_WARPS * 32) lazy_pairs_kernel(PropArgs a) {
         if (lane == 0) a.w.clcnt[v] = CL_DONE;  // decide_kernel: nothing left for this pool
         __syncwarp();
     }
-    if (a.stats) {
-        refp = warp_sum(refp);
+    if (a.stats) {  // (red, refp, pools: warp-uniform; lane 0 adds them)
         if (lane == 0) {
             if (red) atomicAdd((unsigned long long *)&a.stats[GRNND_ST_REDIRECTS], red);
             if (refp) {

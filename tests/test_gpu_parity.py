@@ -333,11 +333,14 @@ def test_exact_only_pair_phase_bit_exact(g, monkeypatch, n, dim, dist, S, R, T1,
     assert np.array_equal(filt.offsets, off) and np.array_equal(filt.neighbor_ids, nb)
 
 
+@pytest.mark.parametrize("force", ["1", "0"])
 @pytest.mark.parametrize("dim", [16, 128, 160])
-def test_filter_degenerate_ties_and_large_norms(g, dim):
+def test_filter_degenerate_ties_and_large_norms(g, monkeypatch, dim, force):
     """Filter stress: exact duplicates (d = 0 = hi, every pair a candidate: the candidate
     queue overflows into the exact sweep) and rows far from the origin (|a|^2 >> d, so the
-    error band is wide)."""
+    error band is wide) -- with the filter forced on, and with the band check (which keeps
+    the exact pair phase for such data)."""
+    monkeypatch.setenv("GRNND_FORCE_FILTER", force)
     r = np.random.default_rng(dim)
     base = r.standard_normal((60, dim)).astype(np.float32)
     dup = base[r.integers(0, 60, 3000)]
@@ -417,3 +420,20 @@ def test_tensor_core_multichunk_bit_exact(g, monkeypatch, dim, R):
         monkeypatch.setenv("GRNND_EXACT_FIRST_ROUNDS", first)
         graph = g.build(ds, g.BuildParams(S=16, R=R, T1=2, T2=4, rho=0.6, seed=5))
         assert np.array_equal(graph.offsets, off) and np.array_equal(graph.neighbor_ids, nb), (dim, R, first)
+
+
+def test_band_check_picks_the_pair_phase(g):
+    """The filter is kept for data whose band is narrow (gaussian: band / distance ~1%) and
+    dropped for data far from the origin relative to its neighbour distances (clustered,
+    shifted): the pools report the measured ratio; both graphs equal the oracle's."""
+    from paper_2510_02774_b200 import builder as B
+
+    for dist, shift, want in (("gaussian", 0.0, True), ("clustered", 0.0, False), ("gaussian", 50.0, False)):
+        ds = generate(6000, 64, dist, seed=2)
+        x = (ds.data + np.float32(shift)).astype(np.float32)
+        st = g.init_neighbors(g.Dataset(x), g.BuildParams(S=16, R=48, T1=2, T2=5, rho=0.6, seed=2))
+        B.run_rounds(st)
+        assert st.pools._filter_ok is want, (dist, shift, st.pools.band_ratio)
+        graph = g.finalize_graph(st)
+        off, nb = oracle.build(x, 16, 48, 2, 5, 0.6, 2)
+        assert np.array_equal(graph.offsets, off) and np.array_equal(graph.neighbor_ids, nb), (dist, shift)

@@ -31,7 +31,7 @@ def run_tcv(*args):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     assert TCV.exists(), "validation library missing: build() compiles it"
-    env = dict(os.environ, GRNND_B200_LIB=str(TCV))
+    env = dict(os.environ, GRNND_B200_LIB=str(TCV), GRNND_FORCE_FILTER="1")  # the filter even where its band is wide
     out = subprocess.run([sys.executable, str(ROOT / "tests" / "tcv_run.py"), *map(str, args)], env=env,
                          capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stderr[-3000:]
