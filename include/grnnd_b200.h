@@ -272,6 +272,13 @@ int grnnd_greedy_search(const int64_t *offsets, const int32_t *nbrs, int64_t n, 
                         int32_t *out_ids, float *out_dists, int64_t *out_cnt, void *visited, size_t visited_bytes,
                         grnnd_stream_t s);
 
+/* refine_accept_loop (_numba_kernels.py:354-381): the sequential oracle's (build_seq,
+ * sequential.py:85-113) accept loop for one vertex on device arrays; ids / dists sorted by
+ * (dist, id), duplicate-free; counts (device int64[2]) = (accepted, redirected). */
+int grnnd_refine_accept_loop(const float *data, int32_t dim, int32_t ld, const int32_t *ids, const float *dists,
+                             int32_t k, int32_t *acc_ids, float *acc_dists, int32_t *red_tgt, int32_t *red_id,
+                             float *red_dist, int64_t *counts, grnnd_stream_t s);
+
 /* Inner-product metric (not in the reference, SURVEY 7 hard part 6): scale each row of
  * data[n, ld] in place to unit L2 norm (sequential fp32 sum of squares, correctly rounded
  * sqrt and division; zero rows unchanged), so squared L2 = 2 - 2<a, b> and the L2 build is

@@ -44,6 +44,7 @@ from .builder import (  # noqa: E402  (loads libgrnnd_b200.so; raises if it is n
     update_round,
     validate_state,
 )
+from .sequential import CandidateList, build_seq, update_neighbors_seq  # noqa: E402
 from .search import (  # noqa: E402
     SearchParams,
     brute_force_knn,
@@ -61,5 +62,5 @@ __all__ = [
     "effective_params", "finalize_graph", "generate", "init_neighbors", "reverse_edge_sampling",
     "rng_redirect_check", "update_round", "validate_params", "validate_state",
     "SearchParams", "brute_force_knn", "brute_force_knn_batch", "greedy_search", "mean_recall", "recall_at_k",
-    "search_batch",
+    "search_batch", "CandidateList", "build_seq", "update_neighbors_seq",
 ]

@@ -101,6 +101,7 @@ _SIGS = {
         C.c_int, [_vp, _vp, _i64, _vp, _i32, _i32, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
     ),
     "grnnd_normalize_rows": (C.c_int, [_vp, _i64, _i32, _i32, _vp]),
+    "grnnd_refine_accept_loop": (C.c_int, [_vp, _i32, _i32, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
 }
 
 if not LIB_PATH.exists():

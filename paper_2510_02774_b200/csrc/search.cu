@@ -521,6 +521,66 @@ int grnnd_greedy_search(const int64_t *offsets, const int32_t *nbrs, int64_t n, 
     return check_launch("greedy_kernel");
 }
 
+// refine_accept_loop (_numba_kernels.py:354-381), the sequential oracle's accept loop for one
+// vertex: candidates in (dist, id) order; a candidate is kept unless an already-kept
+// neighbour lies at or within its distance to the owner (then it is redirected to the FIRST
+// such neighbour with their exact mutual distance).  One warp: the lanes evaluate the kept
+// neighbours 32 at a time, a ballot finds the first hit -- the reference's break.
+__global__ void refine_accept_kernel(const float *__restrict__ data, int32_t ld, int32_t dim,
+                                     const int32_t *__restrict__ ids, const float *__restrict__ dists, int32_t k,
+                                     int32_t *__restrict__ acc_ids, float *__restrict__ acc_dists,
+                                     int32_t *__restrict__ red_tgt, int32_t *__restrict__ red_id,
+                                     float *__restrict__ red_dist, int64_t *__restrict__ counts) {
+    const int lane = lane_id();
+    int na = 0, nr = 0;
+    for (int i = 0; i < k; ++i) {
+        const int32_t cand = ids[i];
+        const float dvn = dists[i];
+        int first = -1;
+        float fd = 0.0f;
+        for (int j0 = 0; j0 < na && first < 0; j0 += 32) {
+            const int j = j0 + lane;
+            float d = 0.0f;
+            if (j < na) d = exact_sqdist_global(data + (int64_t)cand * ld, data + (int64_t)acc_ids[j] * ld, dim);
+            const unsigned hit = __ballot_sync(FULL, j < na && d <= dvn);
+            if (hit) {
+                const int l = __ffs(hit) - 1;
+                first = j0 + l;
+                fd = __shfl_sync(FULL, d, l);
+            }
+        }
+        if (lane == 0) {
+            if (first >= 0) {
+                red_tgt[nr] = acc_ids[first];
+                red_id[nr] = cand;
+                red_dist[nr] = fd;
+            } else {
+                acc_ids[na] = cand;
+                acc_dists[na] = dvn;
+            }
+        }
+        if (first >= 0) ++nr;
+        else ++na;
+        __syncwarp();
+    }
+    if (lane == 0) {
+        counts[0] = na;
+        counts[1] = nr;
+    }
+}
+
+int grnnd_refine_accept_loop(const float *data, int32_t dim, int32_t ld, const int32_t *ids, const float *dists,
+                             int32_t k, int32_t *acc_ids, float *acc_dists, int32_t *red_tgt, int32_t *red_id,
+                             float *red_dist, int64_t *counts, grnnd_stream_t s) {
+    if (dim < 1 || ld < dim || k < 0) {
+        set_error("refine_accept_loop: bad dim/ld/k");
+        return GRNND_EINVAL;
+    }
+    refine_accept_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(s)>>>(data, ld, dim, ids, dists, k, acc_ids,
+                                                                           acc_dists, red_tgt, red_id, red_dist, counts);
+    return check_launch("refine_accept_kernel");
+}
+
 int grnnd_normalize_rows(float *data, int64_t n, int32_t dim, int32_t ld, grnnd_stream_t s) {
     if (n < 0 || dim < 1 || ld < dim) {
         set_error("normalize_rows: bad shape");

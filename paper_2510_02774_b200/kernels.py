@@ -11,8 +11,8 @@ sm_100a kernel through the C ABI, and copies the results back; it is the
 parity surface, not the fast path (``paper_2510_02774_b200.build`` keeps the
 pools resident in HBM instead).
 
-The evaluation kernels brute_force / greedy_search_* run csrc/search.cu;
-refine_accept_loop (the sequential oracle's loop) raises NotImplementedError.
+The evaluation kernels brute_force / greedy_search_* and the sequential oracle's
+refine_accept_loop run csrc/search.cu.
 """
 
 from __future__ import annotations
@@ -249,15 +249,48 @@ def greedy_search_batch(offsets, nbrs, data, queries, L, k, entries):
     return _greedy(offsets, nbrs, data, queries, L, k, entries)
 
 
-def refine_accept_loop(*a, **k):
-    """The sequential RNN-Descent oracle's inner loop (_numba_kernels.py:354-381) belongs to
-    build_seq, which is not part of the parallel build path."""
-    raise NotImplementedError("refine_accept_loop (sequential oracle) is not on the B200 build path")
+_DATA = {"key": None, "dev": None}
+
+
+def _resident(data: np.ndarray) -> torch.Tensor:
+    """Device copy of the dataset for the per-vertex calls of the sequential oracle (one
+    upload per dataset array, not per call; keyed by the array's buffer and shape)."""
+    key = (data.__array_interface__["data"][0], data.shape, data.dtype.str)
+    if _DATA["key"] != key:
+        _DATA["dev"] = upload(np.asarray(data, dtype=np.float32), _dev())
+        _DATA["key"] = key
+    return _DATA["dev"]
+
+
+def refine_accept_loop(data, ids, dists, acc_ids, acc_dists, red_tgt, red_id, red_dist):
+    """_numba_kernels.refine_accept_loop (:354-381): one vertex's sequential accept loop;
+    fills acc_* / red_* in place and returns (accepted, redirected)."""
+    k = int(np.asarray(ids).shape[0])
+    if k == 0:
+        return 0, 0
+    dd = _resident(data)
+    dev = dd.device
+    i_ids = _to(ids, np.int32)
+    i_d = _to(dists, np.float32)
+    out_i = torch.empty((4, k), dtype=torch.int32, device=dev)  # acc_ids, red_tgt, red_id, (spare)
+    out_d = torch.empty((2, k), dtype=torch.float32, device=dev)  # acc_dists, red_dist
+    cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+    _lib.call("grnnd_refine_accept_loop", dd.data_ptr(), int(data.shape[1]), int(dd.shape[1]), i_ids.data_ptr(),
+              i_d.data_ptr(), k, out_i[0].data_ptr(), out_d[0].data_ptr(), out_i[1].data_ptr(), out_i[2].data_ptr(),
+              out_d[1].data_ptr(), cnt.data_ptr(), _stream(dev))
+    na, nr = (int(x) for x in cnt.cpu())
+    oi, od = out_i.cpu().numpy(), out_d.cpu().numpy()
+    acc_ids[:na] = oi[0, :na]
+    acc_dists[:na] = od[0, :na]
+    red_tgt[:nr] = oi[1, :nr]
+    red_id[:nr] = oi[2, :nr]
+    red_dist[:nr] = od[1, :nr]
+    return na, nr
 
 
 __all__ = [
     "hash4_u64", "sqdist", "sample_initial", "init_dists", "gen_update_messages", "gen_reverse_messages",
     "gen_merge_messages", "build_flat", "group_by_target", "apply_grouped_messages", "warmup",
-    "brute_force", "greedy_search_single", "greedy_search_batch",
+    "brute_force", "greedy_search_single", "greedy_search_batch", "refine_accept_loop",
     "padded_ld",
 ]

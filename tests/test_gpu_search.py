@@ -181,3 +181,29 @@ def test_c4_ip_build_equals_oracle_digest(g):
     assert e == od["edges"]
     assert sha(o.astype(np.int64)) == od["sha256_offsets"]
     assert sha(nb[:e].cpu().numpy().astype(np.int32)) == od["sha256_neighbor_ids"]
+
+
+def test_refine_accept_loop_and_build_seq_equal_reference(g, golden):
+    """kernels.refine_accept_loop (_numba_kernels.py:354-381) on the
+    reference's own cases, and build_seq (sequential.py:169-179) graphs, bit for bit."""
+    from paper_2510_02774_b200 import kernels as K
+
+    s = golden("seq")
+    data = s["ral_data"]
+    for t in range(6):
+        ids, dbits = s[f"ral{t}_in"]
+        d = dbits.view(np.float32)
+        kk = ids.shape[0]
+        a_i = np.empty(kk, np.int32); a_d = np.empty(kk, np.float32)
+        r_t = np.empty(kk, np.int32); r_i = np.empty(kk, np.int32); r_d = np.empty(kk, np.float32)
+        na, nr = K.refine_accept_loop(data, ids, d, a_i, a_d, r_t, r_i, r_d)
+        acc, red = s[f"ral{t}_acc"], s[f"ral{t}_red"]
+        assert (na, nr) == (acc.shape[1], red.shape[1]), t
+        assert np.array_equal(a_i[:na], acc[0]) and np.array_equal(a_d[:na].view(np.int32), acc[1])
+        assert np.array_equal(r_t[:nr], red[0]) and np.array_equal(r_i[:nr], red[1])
+        assert np.array_equal(r_d[:nr].view(np.int32), red[2])
+    for name in ("seqA", "seqB"):
+        S, R, T1, T2, seed = (int(x) for x in s[f"{name}_params"])
+        graph = g.build_seq(g.Dataset(s[f"{name}_data"]), g.BuildParams(S=S, R=R, T1=T1, T2=T2, seed=seed))
+        assert np.array_equal(graph.offsets, s[f"{name}_offsets"]), name
+        assert np.array_equal(graph.neighbor_ids, s[f"{name}_nbrs"]), name
