@@ -396,10 +396,11 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     flops = [3 * D * p for p in pairs_ref]
     fp32_tflops = 148 * 128 * 2 * float(sm_mhz) * 1e6 / 1e12  # FMA-counted peak at the sampled clock
     traffic = None
-    try:
-        traffic = json.loads(NCU_FILE.read_text()).get("dram_bytes_per_round")
-    except Exception:
-        pass
+    if args.config == "c2" and (args.n, args.dim) == CONFIGS["c2"][:2]:  # the capture's workload only
+        try:
+            traffic = json.loads(NCU_FILE.read_text()).get("dram_bytes_per_round")
+        except Exception:
+            pass
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
