@@ -6,8 +6,9 @@
 // pools, most pairs redirect) that is 17-29% of all pairs (C2 rounds 1-3).  The exact
 // CUDA-core kernel (pairs.cuh) computes every pair and decide_kernel replays the rule; this
 // kernel IS the rule: a warp owns a pool, stages its rows in shared memory, and visits the
-// anchors in permutation order -- at each live anchor the lanes (= its later partners)
-// compute the reference's exact sequential distance to the anchor in parallel, and the
+// anchors in permutation order -- lane y holds the row of the member at position y in
+// registers, so at each live anchor the lanes after it compute the reference's exact
+// sequential distance to the anchor (a shared-memory broadcast) in parallel, and the
 // anchor's messages and tombstones follow from one ballot (the anchor-serial,
 // partner-parallel formulation is bit-identical).  It emits straight into the message list
 // (keys = source * R + emission index, the reference's order) and marks the pool decided.
@@ -25,7 +26,7 @@ struct LazyWarp {
     float e_d[32];
 };
 
-__global__ void __launch_bounds__(LZ_WARPS * 32) lazy_pairs_kernel(PropArgs a) {
+__global__ void __launch_bounds__(LZ_WARPS * 32, 3) lazy_pairs_kernel(PropArgs a) {
     extern __shared__ __align__(16) unsigned char lz_raw[];
     const int lane = lane_id(), wib = threadIdx.x >> 5;
     LazyWarp &sm = reinterpret_cast<LazyWarp *>(lz_raw)[wib];
@@ -56,35 +57,39 @@ __global__ void __launch_bounds__(LZ_WARPS * 32) lazy_pairs_kernel(PropArgs a) {
         cp_async_wait_all();
         __syncwarp();
 
-        // live[x] over positions (entries are live at the start of the round; TOMB slots dead)
+        // lane y owns the pool member at permutation position y: its row moves to registers
+        // once, so a step reads only the anchor's row from shared memory (a broadcast)
         const int myslot = lane < k ? sm.perm[lane] : 0;
+        float4 mine[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) mine[q] = q < nq ? sm.rows[myslot * LZ_RS4 + q] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float mydv = lane < k ? sm.dv[myslot] : 0.0f;
+        // live[x] over positions (entries are live at the start of the round; TOMB slots dead)
         unsigned live = __ballot_sync(FULL, lane < k && sm.ids[myslot] != TOMB);
         int nm = 0;
         for (int x = 0; x < k - 1; ++x) {
             if (!((live >> x) & 1u)) continue;  // warp-uniform
             const int sa = sm.perm[x];
-            // partner y = x + 1 + lane
-            const int y = x + 1 + lane;
-            const bool py = y < k && ((live >> y) & 1u);
+            const bool py = lane > x && lane < k && ((live >> lane) & 1u);  // partner = position `lane`
             float d = 0.0f;
-            int sb = 0;
             if (py) {
-                sb = sm.perm[y];
-                const float4 *ra = &sm.rows[sa * LZ_RS4], *rb = &sm.rows[sb * LZ_RS4];
-#pragma unroll 4
-                for (int q = 0; q < nq; ++q) {
-                    const float4 u = ra[q], w = rb[q];
-                    d = exact_step(d, u.x, w.x);
-                    d = exact_step(d, u.y, w.y);
-                    d = exact_step(d, u.z, w.z);
-                    d = exact_step(d, u.w, w.w);
+                const float4 *ra = &sm.rows[sa * LZ_RS4];
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    if (q < nq) {
+                        const float4 u = ra[q], w = mine[q];
+                        d = exact_step(d, u.x, w.x);
+                        d = exact_step(d, u.y, w.y);
+                        d = exact_step(d, u.z, w.z);
+                        d = exact_step(d, u.w, w.w);
+                    }
                 }
             }
-            const float dva = sm.dv[sa], dvb = py ? sm.dv[sb] : 0.0f;
+            const float dva = sm.dv[sa], dvb = mydv;
             const bool cond = py && d < (dva >= dvb ? dva : dvb);
             const bool far = cond && !(dvb >= dva);  // the anchor is the farther member
             const unsigned fm = __ballot_sync(FULL, far);
-            const int fl = fm ? __ffs(fm) - 1 : 32;        // lane of the first anchor-far partner
+            const int fl = fm ? __ffs(fm) - 1 : 32;  // position of the first anchor-far partner
             const unsigned vis = __ballot_sync(FULL, py) & (fl < 32 ? (fl == 31 ? FULL : ((2u << fl) - 1u)) : FULL);
             refp += (unsigned long long)__popc(vis);
             const unsigned em = __ballot_sync(FULL, cond && !far) & (fl < 32 ? ((1u << fl) - 1u) : FULL);
@@ -92,14 +97,14 @@ __global__ void __launch_bounds__(LZ_WARPS * 32) lazy_pairs_kernel(PropArgs a) {
             if ((em >> lane) & 1u) {
                 const int j = nm + __popc(em & ((1u << lane) - 1u));
                 sm.e_tgt[j] = sm.ids[sa];
-                sm.e_id[j] = sm.ids[sb];
+                sm.e_id[j] = sm.ids[myslot];
                 sm.e_d[j] = d;
             }
             nm += __popc(em);
-            live &= ~(em << (x + 1));
+            live &= ~em;
             if (fl < 32) {  // the anchor is redirected to its first anchor-far partner and dies
                 if (lane == fl) {
-                    sm.e_tgt[nm] = sm.ids[sb];
+                    sm.e_tgt[nm] = sm.ids[myslot];
                     sm.e_id[nm] = sm.ids[sa];
                     sm.e_d[nm] = d;
                 }
