@@ -131,6 +131,66 @@ __device__ __forceinline__ void apply_range(WarpPool<RPL> &P, const int32_t *__r
     }
 }
 
+// messages [b, e) of a sorted inbox, settled a chunk of 32 at a time while the pool has room:
+// a message is a duplicate of the pool (one shuffle scan) or of an earlier message of its chunk
+// (__match_any), else it is appended -- in order, as the sequential loop would; from the
+// message that would overflow the pool on, the ordered insert() (replacement order matters)
+template <int RPL>
+__device__ __forceinline__ void apply_range_bulk(WarpPool<RPL> &P, const int32_t *__restrict__ iid,
+                                                 const float *__restrict__ idist, int64_t b, int64_t e, Outcome &oc,
+                                                 int32_t *s_id, float *s_d) {
+    const int lane = lane_id();
+    int64_t c = b;
+    bool serial = false;
+    for (; c < e && !serial; c += 32) {
+        const int nch = (int)(e - c < 32 ? e - c : 32);
+        const bool live = lane < nch;
+        const int32_t x = live ? iid[c + lane] : -2 - lane;  // dead lanes: distinct non-ids
+        const float xd = live ? idist[c + lane] : 0.0f;
+        bool dup = false;
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+            const int lim = min(32, P.cnt - r * 32);  // warp-uniform
+            for (int jj = 0; jj < lim; ++jj) dup |= __shfl_sync(FULL, P.id[r], jj) == x;
+        }
+        const unsigned peers = __match_any_sync(FULL, x);
+        dup = live && (dup || (peers & ((1u << lane) - 1u)) != 0u);
+        const unsigned addm = __ballot_sync(FULL, live && !dup), dupm = __ballot_sync(FULL, dup);
+        const int room = P.cap - P.cnt;
+        int nbulk = nch;
+        if (__popc(addm) > room) {  // the (room+1)-th append overflows: bulk stops before it
+            unsigned mm = addm;
+            for (int t = 0; t < room; ++t) mm &= mm - 1u;
+            nbulk = __ffs(mm) - 1;
+            serial = true;
+        }
+        const unsigned pre = nbulk >= 32 ? 0xFFFFFFFFu : ((1u << nbulk) - 1u);
+        const int nadd = __popc(addm & pre);
+        if (lane < nbulk && live && !dup) {
+            const int p = P.cnt + __popc(addm & ((1u << lane) - 1u));
+            s_id[p] = x;
+            s_d[p] = xd;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+            const int q = r * 32 + lane;
+            if (q >= P.cnt && q < P.cnt + nadd) {
+                P.id[r] = s_id[q];
+                P.d[r] = s_d[q];
+            }
+        }
+        __syncwarp();
+        if (nadd) P.mxv = false;
+        P.cnt += nadd;
+        oc.ins += (unsigned long long)nadd;
+        oc.dup += (unsigned long long)__popc(dupm & pre);
+        for (int j = nbulk; j < nch; ++j)  // only after an overflow
+            P.insert(__shfl_sync(FULL, x, j), __shfl_sync(FULL, xd, j), oc);
+    }
+    apply_range<RPL>(P, iid, idist, c, e, oc);  // the pool is full: the ordered insert
+}
+
 template <int RPL>
 __global__ void __launch_bounds__(256) apply_round_kernel(ApplyArgs a) {
     __shared__ int32_t s_id[8][RPL * 32];
@@ -146,21 +206,24 @@ __global__ void __launch_bounds__(256) apply_round_kernel(ApplyArgs a) {
         // split point: messages from sources < tg come first (key = src * cap + j)
         int64_t split = e;
         if (!a.own_after_all) {
-            // segment is sorted by key; first index with key >= tg * cap
+            // segment is sorted by key; first index with key >= tg * cap: 32 keys per coalesced
+            // load and a ballot (a binary search was a chain of dependent global loads)
             const int64_t lim = tg * (int64_t)cap;
-            int64_t lo_i = b, hi_i = e;
-            while (lo_i < hi_i) {
-                const int64_t mid = (lo_i + hi_i) >> 1;
-                if (a.w.i_key[mid] < lim) lo_i = mid + 1;
-                else hi_i = mid;
+            split = e;
+            for (int64_t c0 = b; c0 < e; c0 += 32) {
+                const bool below = c0 + lane < e && a.w.i_key[c0 + lane] < lim;
+                const unsigned bl = __ballot_sync(FULL, below);
+                if (bl != FULL) {
+                    split = c0 + __popc(bl);
+                    break;
+                }
             }
-            split = lo_i;
         }
         WarpPool<RPL> P;
         P.cnt = 0;
         P.cap = cap;
         P.mxv = false;
-        apply_range<RPL>(P, a.w.i_id, a.w.i_dist, b, split, oc);
+        apply_range_bulk<RPL>(P, a.w.i_id, a.w.i_dist, b, split, oc, s_id[wib], s_d[wib]);
         // own entries (survivors / merge) in slot order
         const int k = a.read_count[t];
         const int32_t *rid = a.read_ids + t * cap;
@@ -270,7 +333,7 @@ __global__ void __launch_bounds__(256) apply_round_kernel(ApplyArgs a) {
                 }
             }
         }
-        apply_range<RPL>(P, a.w.i_id, a.w.i_dist, split, e, oc);
+        apply_range_bulk<RPL>(P, a.w.i_id, a.w.i_dist, split, e, oc, s_id[wib], s_d[wib]);
         __syncwarp();  // in place: every lane's reads of the row precede the stores
         P.store(a.write_ids + t * cap, a.write_dists + t * cap);
         if (lane == 0) {
