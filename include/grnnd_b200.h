@@ -170,6 +170,9 @@ typedef struct {
     const float *norms; /* fp32 [n_total] squared row norms (grnnd_row_norms) enabling the
                            filtered pair phase, or NULL for the exact-only pair phase; the
                            built graph is the same either way                              */
+    int32_t filter_split; /* 1: the tensor-core Gram as hi*hi + hi*lo + lo*hi (split TF32,
+                           ~fp32 accurate: a band 2^7 narrower) for data far from the origin
+                           relative to its neighbour distances; 0: plain TF32            */
 } grnnd_pools;
 
 /* Squared L2 norm of every row of data[n, ld] (first dim columns) into out[n] (device).

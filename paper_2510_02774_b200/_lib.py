@@ -57,6 +57,7 @@ class Pools(C.Structure):
         ("msg_capacity", _i64),
         ("stats", _vp),
         ("norms", _vp),
+        ("filter_split", _i32),
     ]
 
 

@@ -276,7 +276,8 @@ class _DevicePools:
                 _lib.call("grnnd_row_norms", self.data.data_ptr(), self.n_total, self.dim, self.ld,
                           self.norms.data_ptr(), _stream(self.dev))
 
-    def struct(self, stats: torch.Tensor | None = None, filtered: bool = True) -> _lib.Pools:
+    def struct(self, stats: torch.Tensor | None = None, filtered: "bool | int" = True) -> _lib.Pools:
+        """filtered: False / 0 exact pair phase, True / 1 TF32 filter, 2 split-TF32 filter."""
         norms = self.norms if filtered else None
         return _lib.Pools(
             self.data.data_ptr(), self.n_total, self.lo, self.hi, self.dim, self.ld, self.cap,
@@ -285,30 +286,38 @@ class _DevicePools:
             self.workspace.data_ptr(), self.workspace.numel(), self.msg_capacity,
             (stats if stats is not None else self.scratch_stats).data_ptr(),
             norms.data_ptr() if norms is not None else None,
+            1 if (filtered == 2 and norms is not None) else 0,
         )
 
-    BAND_LIMIT = 0.05  # filter band / mean stored distance above which the filter is not used
+    BAND_LIMIT = 0.05  # filter band / mean stored distance above which plain TF32 is not used
 
-    def filtered_round(self, stream_id: int) -> bool:
+    def filtered_round(self, stream_id: int) -> int:
         """Pair-phase mode of an update round.  The first rounds start from random pools,
         where most pairs meet the redirect condition (68% / 32% / 17% of all pairs in rounds
         1-3 at C2) and the tensor-core filter settles few of them: those rounds run the
-        exact-only pair phase; later rounds the filtered one -- unless the filter's error band
-        (2^-8 (|a|^2 + |b|^2)) is wide against the pools' distances, i.e. the
-        data lie far from the origin relative to their neighbour distances (clustered data:
-        85% of pairs would be candidates).  That is measured once, at the first filtered
-        round (one host read per build).  Same graph either way."""
+        exact-only pair phase; later rounds the filtered one.  The plain TF32 filter's error
+        band (2^-8 (|a|^2 + |b|^2)) is wide when the data lie far from the origin
+        relative to their neighbour distances (clustered data: 85% of pairs would be
+        candidates); such builds keep the exact pair phase.  (The split-TF32 Gram, band
+        2^-15 (|a|^2 + |b|^2), settles those pairs -- candidates drop to the redirect-capable
+        ones -- but its three MMAs per k-block made it slower than the exact tile kernel on
+        C2c; GRNND_FORCE_FILTER=2 selects it.)  The band is measured once, at the first
+        filtered round (one host read per build).  Returns 0 (exact), 1 (TF32) or 2 (split
+        TF32); the graph is the same either way."""
         if stream_id <= int(os.environ.get("GRNND_EXACT_FIRST_ROUNDS", EXACT_FIRST_ROUNDS)):
-            return False
-        if self.norms is None or os.environ.get("GRNND_FORCE_FILTER") == "1":
-            return self.norms is not None
+            return 0
+        if self.norms is None:
+            return 0
+        force = os.environ.get("GRNND_FORCE_FILTER")  # tests / A-B runs: 0 exact, 1 TF32, 2 split
+        if force in ("0", "1", "2"):
+            return int(force)
         if self._filter_ok is None:
             out = torch.zeros(2, dtype=torch.float64, device=self.dev)
             with torch.cuda.device(self.dev):
                 _lib.call("grnnd_band_terms", C.byref(self.struct()), out.data_ptr(), _stream(self.dev))
             sr, cnt = (float(x) for x in out.cpu())
             self.band_ratio = 2.0 ** -7 * sr / max(cnt, 1.0)  # mean band / stored distance
-            self._filter_ok = self.band_ratio <= self.BAND_LIMIT
+            self._filter_ok = 1 if self.band_ratio <= self.BAND_LIMIT else 0
         return self._filter_ok
 
     def swap(self) -> None:

@@ -347,6 +347,7 @@ static int emit_update(const grnnd_pools *p, const Workspace &w, uint64_t seed, 
     a.w = w;
     a.stats = p->stats;
     a.norms = p->norms;
+    a.split = p->filter_split;
     filter_eps(p->dim, &a.eps_n, &a.eps_h);
     return launch_propagate(a, st);
 }

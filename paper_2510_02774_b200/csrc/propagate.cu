@@ -667,14 +667,18 @@ static int launch_tc_pairs(const PropArgs &a, int bin, cudaStream_t st) {
 template <int SZ>
 static int launch_tc3_pairs(const PropArgs &a, int bin, cudaStream_t st) {
     const bool multi = a.dim > 128;
+    const bool split = !multi && a.split;
     if (multi && device_sm_count() > T3Q_CTAS) {
         set_error("tc3: %d SMs > %d overflow-queue slots", device_sm_count(), T3Q_CTAS);
         return GRNND_EUNSUPPORTED;
     }
-    auto kern = multi ? tc3_pairs_kernel<SZ, true> : tc3_pairs_kernel<SZ, false>;
-    const size_t smem = (size_t)T3_NS * T3_STAGE + T3_PAD + (multi ? sizeof(T3Smem<SZ, true>) : sizeof(T3Smem<SZ, false>)) + 1024;
-    static SmemOptIn optin[2];  // one per kernel
-    GRNND_CUDA(optin[multi ? 1 : 0].ensure(kern, smem));
+    auto kern = multi ? tc3_pairs_kernel<SZ, true, false>
+                      : split ? tc3_pairs_kernel<SZ, false, true> : tc3_pairs_kernel<SZ, false, false>;
+    const size_t smem = split ? (size_t)T3_NS_SPLIT * T3_STAGE + T3_RING + T3_PAD + sizeof(T3Smem<SZ, false>) + 1024
+                              : (size_t)T3_NS * T3_STAGE + T3_PAD +
+                                    (multi ? sizeof(T3Smem<SZ, true>) : sizeof(T3Smem<SZ, false>)) + 1024;
+    static SmemOptIn optin[3];  // one per kernel
+    GRNND_CUDA(optin[multi ? 1 : split ? 2 : 0].ensure(kern, smem));
     kern<<<device_sm_count(), T3_NT, smem, st>>>(a, bin);
     return check_launch("tc3_pairs_kernel");
 }

@@ -28,6 +28,7 @@ struct PropArgs {
     // exact-only pair phase; eps_n / eps_h are the filter's error-bound coefficients
     const float *norms;
     float eps_n, eps_h;
+    int32_t split;  // tensor-core Gram in split TF32 (tc3_pairs.cuh SPLIT)
 };
 
 // error-bound coefficients of the filtered pair phase for dimension dim

@@ -28,6 +28,12 @@ constexpr int T3_ROWS = 96;
 constexpr int T3_KB = T3_ROWS * 128;  // one 32-dim k-block of a stage (12 KB)
 constexpr int T3_STAGE = 4 * T3_KB;   // 96 rows x 128 fp32 (48 KB)
 constexpr int T3_NS = 4;              // row stages
+// SPLIT (data far from the origin): the Gram as hi*hi + hi*lo + lo*hi with hi = the row
+// truncated to TF32 and lo = row - hi (both exact in fp32, converted per k-block into a
+// 2-slot ring by the MMA warp); 3 row stages make room for the ring
+constexpr int T3_NS_SPLIT = 3;
+constexpr int T3_RING = 2 * 2 * T3_KB;  // 2 slots x (hi, lo) k-blocks
+constexpr float TC_EPS_SPLIT = 3.0517578125e-05f;  // 2^-15 (~3x the split bound)
 #ifndef GRNND_T3_NM
 #define GRNND_T3_NM 6
 #endif
@@ -85,7 +91,7 @@ struct T3Smem {
     // second pair's row starts 132 floats in, so the two summing lanes read distinct banks)
     static constexpr int PSQW = MULTI ? 2 * 132 : 2 * 128;
     alignas(16) float psq[6 * PSQW];
-    uint64_t mfull[T3_NM], mempty[T3_NM], full[T3_NS], empty[T3_NS], accf[2], acce[2], qrdy[2], qemp[2];
+    uint64_t mfull[T3_NM], mempty[T3_NM], full[T3_NS], empty[T3_NS], accf[2], acce[2], qrdy[2], qemp[2], rfree[2];
     uint32_t tmem_base;
 };
 
@@ -151,16 +157,18 @@ __device__ long long g_t3trace[64][10];  // CTA 0: per group event times (profil
 // 128 dims; the MMA accumulates the chunks' Grams in the same TMEM accumulator and releases
 // each stage with tcgen05.commit (the exact sets never hold a stage); the exact chains read
 // the candidate pairs' rows from global memory (L2: the group's rows were just streamed).
-template <int SZ, bool MULTI>
+template <int SZ, bool MULTI, bool SPLIT>
 __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin) {
     using S = T3Smem<SZ, MULTI>;
     constexpr int GP = S::GP;
     constexpr int R = T3_ROWS;
-    constexpr int NS = T3_NS;
+    constexpr int NS = SPLIT ? T3_NS_SPLIT : T3_NS;
+    constexpr float EPS_TC = SPLIT ? TC_EPS_SPLIT : TC_EPS;
     constexpr int NM = T3_NM;
     extern __shared__ __align__(1024) unsigned char t3_raw[];
     unsigned char *base = t3_raw + ((1024 - (tc::smem_u32(t3_raw) & 1023)) & 1023);
-    S &sm = *reinterpret_cast<S *>(base + NS * T3_STAGE + T3_PAD);
+    unsigned char *ring = base + NS * T3_STAGE;  // SPLIT only
+    S &sm = *reinterpret_cast<S *>(base + NS * T3_STAGE + (SPLIT ? T3_RING : 0) + T3_PAD);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #ifdef GRNND_T3_PROF
@@ -195,6 +203,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             tc::mbar_init(&sm.empty[s], MULTI ? 1 : 3);  // MULTI: the MMA's commit frees a stage
         }
         for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&sm.rfree[b], 1);
             tc::mbar_init(&sm.accf[b], 1);
             tc::mbar_init(&sm.acce[b], T3_NF / 32);
             tc::mbar_init(&sm.qrdy[b], T3_NF / 32);
@@ -272,6 +281,54 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
 #endif
             }
         }
+    } else if (warp == 1 && SPLIT) {
+        // ================= split-TF32 MMA (the whole warp converts, lane 0 issues) =================
+        for (int64_t g = 0; g < nmine; ++g) {
+            const int s = (int)(g % NS), m = (int)(g % NM), ac = (int)(g & 1);
+            tc::mbar_wait(&sm.full[s], (uint32_t)((g / NS) & 1));
+            tc::mbar_wait(&sm.mfull[m], (uint32_t)((g / NM) & 1));
+            tc::mbar_wait(&sm.acce[ac], (uint32_t)(((g >> 1) & 1) ^ 1));
+            tc::fence_after();
+            const int n = GP == 1 ? ((sm.meta[m].hdr[0].y + 15) / 16 * 16) : R;
+            const uint32_t idesc = tc::idesc_tf32(n < 16 ? 16 : n);
+            const uint32_t d = tmem + (uint32_t)(ac * 128);
+#pragma unroll 1
+            for (int kb = 0; kb < 4; ++kb) {
+                const int64_t u = g * 4 + kb;
+                const int slot = (int)(u & 1);
+                tc::mbar_wait(&sm.rfree[slot], (uint32_t)(((u >> 1) & 1) ^ 1));  // MMAs of u - 2 done
+                const float4 *src = reinterpret_cast<const float4 *>(base + s * T3_STAGE + kb * T3_KB);
+                float4 *hi = reinterpret_cast<float4 *>(ring + slot * 2 * T3_KB);
+                float4 *lo = hi + T3_KB / 16;
+                for (int e = lane; e < T3_KB / 16; e += 32) {  // same (swizzled) layout as the stage
+                    const float4 v = src[e];
+                    float4 h;
+                    h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                    h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                    h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                    h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                    hi[e] = h;
+                    lo[e] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);  // exact
+                }
+                tc::fence_proxy_async();  // generic writes -> tensor-core reads
+                __syncwarp();
+                if (lane == 0) {
+                    tc::fence_after();
+                    const uint32_t ha = tc::smem_u32(hi), la = tc::smem_u32(lo);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint64_t dh = tc::sw128_desc(ha + kk * 32), dl = tc::sw128_desc(la + kk * 32);
+                        tc::mma_tf32(d, dh, dh, idesc, (kb | kk) != 0);
+                        tc::mma_tf32(d, dh, dl, idesc, 1u);
+                        tc::mma_tf32(d, dl, dh, idesc, 1u);
+                    }
+                    tc::mma_commit(&sm.rfree[slot]);
+                }
+                __syncwarp();
+            }
+            if (lane == 0) tc::mma_commit(&sm.accf[ac]);
+            __syncwarp();
+        }
     } else if (warp == 1) {
         // ================= MMA issuer =================
         if (lane == 0) {
@@ -328,7 +385,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 const int p = i / SZ, sl = i - p * SZ;
                 const bool live = sl < mt.hdr[p].y && mt.ids[i] != TOMB;
                 const float nr = mt.nrm[i];
-                float A = nr * (1.0f - TC_EPS);
+                float A = nr * (1.0f - EPS_TC);
                 if (!(nr <= 1.0e37f)) A = -INFINITY;  // rearranged test could overflow: always a candidate
                 const float2 t = live ? make_float2(A, fmaf(mt.dv[i], 1.0f + eps_h, 1e-30f)) : make_float2(0.0f, -1.0f);
                 sm.ab[b][i] = t;
@@ -419,7 +476,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                         }
                         const float nn = mt.nrm[i] + mt.nrm[jr];
                         const float err = fabsf(fmaf(-2.0f, __uint_as_float(r[c]), nn) - dx);
-                        const float ratio = err / fmaf(TC_EPS, nn, 1e-30f);
+                        const float ratio = err / fmaf(EPS_TC, nn, 1e-30f);
                         worst = ratio > worst ? ratio : worst;
                         bad += ratio > 1.0f ? 1ull : 0ull;
                         ++chk;

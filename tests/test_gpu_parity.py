@@ -423,17 +423,32 @@ def test_tensor_core_multichunk_bit_exact(g, monkeypatch, dim, R):
 
 
 def test_band_check_picks_the_pair_phase(g):
-    """The filter is kept for data whose band is narrow (gaussian: band / distance ~1%) and
-    dropped for data far from the origin relative to its neighbour distances (clustered,
-    shifted): the pools report the measured ratio; both graphs equal the oracle's."""
+    """The plain TF32 filter is kept for data whose band is narrow (gaussian: band /
+    distance ~1%); data far from the origin relative to its neighbour distances (clustered,
+    shifted) keep the exact pair phase: the pools report the measured ratio; every graph
+    equals the oracle's."""
     from paper_2510_02774_b200 import builder as B
 
-    for dist, shift, want in (("gaussian", 0.0, True), ("clustered", 0.0, False), ("gaussian", 50.0, False)):
+    for dist, shift, want in (("gaussian", 0.0, 1), ("clustered", 0.0, 0), ("gaussian", 50.0, 0)):
         ds = generate(6000, 64, dist, seed=2)
         x = (ds.data + np.float32(shift)).astype(np.float32)
         st = g.init_neighbors(g.Dataset(x), g.BuildParams(S=16, R=48, T1=2, T2=5, rho=0.6, seed=2))
         B.run_rounds(st)
-        assert st.pools._filter_ok is want, (dist, shift, st.pools.band_ratio)
+        assert st.pools._filter_ok == want, (dist, shift, st.pools.band_ratio)
         graph = g.finalize_graph(st)
         off, nb = oracle.build(x, 16, 48, 2, 5, 0.6, 2)
         assert np.array_equal(graph.offsets, off) and np.array_equal(graph.neighbor_ids, nb), (dist, shift)
+
+
+@pytest.mark.parametrize("mode", ["2", "0"])
+@pytest.mark.parametrize("dist,shift,R", [("clustered", 0.0, 96), ("gaussian", 300.0, 40), ("gaussian", 0.0, 24),
+                                          ("uniform", 0.0, 64)])
+def test_split_tf32_filter_bit_exact(g, monkeypatch, dist, shift, R, mode):
+    """The split-TF32 Gram (hi*hi + hi*lo + lo*hi, band 2^-15 (|a|^2 + |b|^2)) and the exact
+    pair phase forced on near- and far-from-origin data: the oracle's graph bit for bit."""
+    monkeypatch.setenv("GRNND_FORCE_FILTER", mode)
+    ds = generate(5000, 128, dist, seed=7)
+    x = (ds.data + np.float32(shift)).astype(np.float32)
+    graph = g.build(g.Dataset(x), g.BuildParams(S=16, R=R, T1=2, T2=5, rho=0.6, seed=7))
+    off, nb = oracle.build(x, 16, R, 2, 5, 0.6, 7)
+    assert np.array_equal(graph.offsets, off) and np.array_equal(graph.neighbor_ids, nb)

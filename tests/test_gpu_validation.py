@@ -27,11 +27,11 @@ ROOT = Path(__file__).resolve().parents[1]
 TCV = ROOT / "paper_2510_02774_b200" / "_build" / "libgrnnd_b200_tcv.so"
 
 
-def run_tcv(*args):
+def run_tcv(*args, force="1"):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     assert TCV.exists(), "validation library missing: build() compiles it"
-    env = dict(os.environ, GRNND_B200_LIB=str(TCV), GRNND_FORCE_FILTER="1")  # the filter even where its band is wide
+    env = dict(os.environ, GRNND_B200_LIB=str(TCV), GRNND_FORCE_FILTER=force)  # the filter even where its band is wide
     out = subprocess.run([sys.executable, str(ROOT / "tests" / "tcv_run.py"), *map(str, args)], env=env,
                          capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stderr[-3000:]
@@ -48,6 +48,21 @@ def run_tcv(*args):
 def test_tensor_core_bound_holds_and_graph_exact(n, dim, R, T1, T2, dist):
     r = run_tcv(n, dim, R, T1, T2, dist)
     assert r["lib"].endswith("libgrnnd_b200_tcv.so")
+    assert r["checked"] > 0
+    assert r["violations"] == 0, r
+    assert r["max_ratio"] < 1.0
+    off, nb = oracle.build(generate(n, dim, dist, seed=1).data, 20, R, T1, T2, 0.6, 1)
+    assert np.array_equal(np.array(r["offsets"]), off) and np.array_equal(np.array(r["nbrs"]), nb)
+
+
+@pytest.mark.parametrize("n,dim,R,T1,T2,dist", [
+    (8000, 128, 96, 2, 6, "clustered"),   # far from the origin: the split-TF32 Gram's case
+    (6000, 64, 40, 2, 5, "gaussian"),
+])
+def test_split_tf32_bound_holds_and_graph_exact(n, dim, R, T1, T2, dist):
+    """The split-TF32 Gram's error against its band 2^-15 (|a|^2 + |b|^2), on every screened
+    pair: 0 violations, the largest error well inside the band."""
+    r = run_tcv(n, dim, R, T1, T2, dist, force="2")
     assert r["checked"] > 0
     assert r["violations"] == 0, r
     assert r["max_ratio"] < 1.0
