@@ -271,6 +271,16 @@ __device__ __forceinline__ uint64_t bits_below(int f, int w) {  // bits of word 
     return (1ull << b) - 1ull;
 }
 
+// bit x of a multi-word mask without a runtime index into the array (which would put it in
+// local memory): every word is compared against x's word
+template <int MW>
+__device__ __forceinline__ bool mask_bit(const uint64_t (&m)[MW], int x) {
+    uint64_t w = 0ull;
+#pragma unroll
+    for (int i = 0; i < MW; ++i) w = (x >> 6) == i ? m[i] : w;
+    return (w >> (x & 63)) & 1ull;
+}
+
 // warps per decide CTA: 8 (R <= 128), 4 for the wider rows (static shared memory <= 48 KB)
 template <int MW>
 constexpr int dec_warps() { return MW <= 2 ? 8 : 4; }
@@ -324,7 +334,7 @@ __device__ __forceinline__ void decide_pool(const PropArgs &a, int k, int64_t v,
         masks(x, c, am);
         int cur = x0;
         while (true) {
-            const bool mylive = x < k - 1 && ((live[x >> 6] >> (x & 63)) & 1ull);
+            const bool mylive = x < k - 1 && mask_bit<MW>(live, x);
             bool hit = false;
 #pragma unroll
             for (int i = 0; i < MW; ++i) hit |= (c[i] & live[i]) != 0ull;
@@ -387,7 +397,9 @@ __device__ __forceinline__ void decide_pool(const PropArgs &a, int k, int64_t v,
                     e_key[base] = (uint16_t)((xa << 8) | f);
                 }
                 ++base;
-                live[xa >> 6] &= ~(1ull << (xa & 63));
+#pragma unroll
+                for (int i = 0; i < MW; ++i)
+                    if ((xa >> 6) == i) live[i] &= ~(1ull << (xa & 63));
             }
             nm = base;
             cur = xa + 1;
@@ -439,7 +451,7 @@ __device__ __forceinline__ void decide_pool(const PropArgs &a, int k, int64_t v,
         bool alive = false;
         if (s < k) {
             const int x = pos[s];
-            alive = (live[x >> 6] >> (x & 63)) & 1ull;
+            alive = mask_bit<MW>(live, x);
             if (!alive && ids[s] != TOMB) a.read_ids[v * cap + s] = TOMB;
             alive = alive && ids[s] != TOMB;
         }
