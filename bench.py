@@ -284,13 +284,21 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     from paper_2510_02774_b200 import _lib
     from paper_2510_02774_b200.builder import DeviceBuild, upload
 
+    # (functional multi-rank test on one GPU: GRNND_SHARE_GPU=1 puts every rank on cuda:0 and
+    # GRNND_DIST_BACKEND=gloo replaces NCCL, which refuses two ranks on one device)
+    if os.environ.get("GRNND_SHARE_GPU") == "1":
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("GRNND_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if dist is not None:
@@ -363,6 +371,16 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
         def api_build(d, p):
             return g.build(d, p, metric=args.metric_kind)
     graph = api_build(pinned_ds, params)  # warm the device and pinned-host allocators for this path
+    sharded_parity = None
+    if world > 1 and rank == 0:  # the gathered multi-rank graph against the reference digest
+        so = hashlib.sha256(np.ascontiguousarray(graph.offsets, dtype=np.int64).tobytes()).hexdigest()
+        sn = hashlib.sha256(np.ascontiguousarray(graph.neighbor_ids, dtype=np.int32).tobytes()).hexdigest()
+        sharded_parity = {"sha256_offsets": so, "sha256_neighbor_ids": sn, "digest_match": None}
+        f = ROOT / "tests" / "golden" / f"{args.config}_reference.npz"
+        if args.config in CONFIGS and CONFIGS[args.config][:2] == (args.n, args.dim) and f.exists():
+            meta = json.loads(str(np.load(f)["meta"]))
+            sharded_parity["digest_match"] = so == meta["sha256_offsets"] and sn == meta["sha256_neighbor_ids"]
+            sharded_parity["reference"] = "numba reference build (tests/golden/make_reference_digest.py)"
     e2e = []
     for _ in range(args.steps):
         del graph  # a caller keeps one graph at a time: its host blocks are reused
@@ -402,6 +420,8 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
         except Exception:
             pass
 
+    if sharded_parity is not None:
+        parity = sharded_parity
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         if args.n * args.dim <= 1_000_000 * 128:
@@ -421,7 +441,10 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (numpy default_rng(1).standard_normal, the reference's generate recipe)",
             "config": config_of(args),
-            "parallelism": f"shard{world} (ID-range ownership, NCCL all-to-all per round)" if world > 1 else "single",
+            "parallelism": (f"shard{world} (ID-range ownership, {os.environ.get('GRNND_DIST_BACKEND', 'nccl').upper()} "
+                            f"all-to-all per round"
+                            + (", all ranks on one GPU: functional run" if os.environ.get("GRNND_SHARE_GPU") == "1" else "")
+                            + ")") if world > 1 else "single",
             "mvec_per_s": round(args.n / value / 1e6, 3),
             "edges": edges,
             "clocks": clk.summary(),

@@ -132,6 +132,13 @@ def exchange_all_to_all(out: torch.Tensor, send_counts: list[int], inb: torch.Te
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
+    if out.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo's all-to-all moves host tensors: stage through the host (functional multi-rank
+        # runs on one GPU, where NCCL refuses two ranks per device)
+        inb_h = torch.empty(inb.shape, dtype=inb.dtype)
+        n_in = exchange_all_to_all(out.cpu(), send_counts, inb_h, group)
+        inb[:n_in].copy_(inb_h[:n_in])
+        return n_in
     dev = out.device
     sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
     rc = torch.empty(world, dtype=torch.int64, device=dev)
