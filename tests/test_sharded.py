@@ -198,3 +198,48 @@ def test_message_overflow_is_reported():
     ds = generate(3000, 16, "gaussian", seed=1)
     with pytest.raises(g.DeviceError):
         build_virtual_shards(ds, g.BuildParams(S=16, R=32, T1=2, T2=2, seed=1), 2, msg_capacity=2000)
+
+
+def _gpu_worker(rank, world, port, cfg, out_q):
+    """One rank of a real multi-process sharded build on the GPU (ranks share cuda:0 over
+    gloo: NCCL refuses two ranks on one device); the public build_sharded API."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2510_02774_b200 as g
+        from paper_2510_02774_b200.sharded import build_sharded
+
+        n, dim, dist_name, S, R, T1, T2, seed = cfg
+        ds = generate(n, dim, dist_name, seed=seed)
+        log = []
+        graph = build_sharded(ds, g.BuildParams(S=S, R=R, T1=T1, T2=T2, rho=0.6, seed=seed), report_stats=log)
+        if rank == 0:
+            out_q.put((graph.offsets, graph.neighbor_ids, [s.redirects for s in log]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,cfg", [(2, (6000, 64, "gaussian", 16, 48, 2, 5, 3)),
+                                       (3, (4000, 32, "clustered", 12, 24, 2, 4, 5))])
+def test_multi_process_sharded_build_gpu_bit_exact(world, cfg):
+    """build_sharded in `world` separate processes (the exchange, the sharded pair phase and
+    apply, the graph gather): the oracle's graph and per-round redirect counts."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, cfg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    off, nb, red = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    n, dim, dist_name, S, R, T1, T2, seed = cfg
+    want_off, want_nb, st = oracle.build(generate(n, dim, dist_name, seed=seed).data, S, R, T1, T2, 0.6, seed,
+                                         with_stats=True)
+    assert np.array_equal(off, want_off) and np.array_equal(nb, want_nb)
+    assert red == st[:, 2].tolist()
