@@ -39,6 +39,27 @@ __device__ __forceinline__ float exact_step(float s, float a, float b) {
     return __fadd_rn(s, __fmul_rn(d, d));
 }
 
+// Four consecutive exact_steps (dims x, y, z, w in order).  The differences and squares go
+// through the packed f32x2 pipes (FADD2 / FMUL2: each lane rounded like __fsub_rn / __fmul_rn;
+// a - b == a + (-b) exactly in IEEE arithmetic); the running sum stays scalar and sequential,
+// so nothing can be contracted into an FMA and the bits equal four exact_steps.
+__device__ __forceinline__ float2 sq2(float a0, float a1, float b0, float b1) {
+    const float2 d = __fadd2_rn(make_float2(a0, a1), make_float2(-b0, -b1));
+    return __fmul2_rn(d, d);
+}
+__device__ __forceinline__ float exact_step4(float s, const float4 &a, const float4 &b) {
+    const float2 p0 = sq2(a.x, a.y, b.x, b.y), p1 = sq2(a.z, a.w, b.z, b.w);
+    s = __fadd_rn(s, p0.x);
+    s = __fadd_rn(s, p0.y);
+    s = __fadd_rn(s, p1.x);
+    return __fadd_rn(s, p1.y);
+}
+// the four squared differences alone (exact_step(0, a, b) == (a - b)^2: adding +0 is exact)
+__device__ __forceinline__ float4 sq4(const float4 &a, const float4 &b) {
+    const float2 p0 = sq2(a.x, a.y, b.x, b.y), p1 = sq2(a.z, a.w, b.z, b.w);
+    return make_float4(p0.x, p0.y, p1.x, p1.y);
+}
+
 // Sequential exact distance between two global rows (used off the hot loop).
 __device__ __forceinline__ float exact_sqdist_global(const float* __restrict__ a,
                                                      const float* __restrict__ b, int32_t dim) {
@@ -48,10 +69,7 @@ __device__ __forceinline__ float exact_sqdist_global(const float* __restrict__ a
         for (; d + 4 <= dim; d += 4) {
             float4 x = __ldg(reinterpret_cast<const float4*>(a + d));
             float4 y = __ldg(reinterpret_cast<const float4*>(b + d));
-            s = exact_step(s, x.x, y.x);
-            s = exact_step(s, x.y, y.y);
-            s = exact_step(s, x.z, y.z);
-            s = exact_step(s, x.w, y.w);
+            s = exact_step4(s, x, y);
         }
     }
     for (; d < dim; ++d) s = exact_step(s, __ldg(a + d), __ldg(b + d));

@@ -78,10 +78,7 @@ __global__ void __launch_bounds__(LZ_WARPS * 32, 3) lazy_pairs_kernel(PropArgs a
                 for (int q = 0; q < 32; ++q) {
                     if (q < nq) {
                         const float4 u = ra[q], w = mine[q];
-                        d = exact_step(d, u.x, w.x);
-                        d = exact_step(d, u.y, w.y);
-                        d = exact_step(d, u.z, w.z);
-                        d = exact_step(d, u.w, w.w);
+                        d = exact_step4(d, u, w);
                     }
                 }
             }

@@ -108,10 +108,7 @@ __device__ __forceinline__ float exact_sqdist_smem(const float4 *__restrict__ a,
     float s = 0.0f;
     for (int q = 0; q < nq; ++q) {
         const float4 x = a[q], y = b[q];
-        s = exact_step(s, x.x, y.x);
-        s = exact_step(s, x.y, y.y);
-        s = exact_step(s, x.z, y.z);
-        s = exact_step(s, x.w, y.w);
+        s = exact_step4(s, x, y);
     }
     return s;
 }

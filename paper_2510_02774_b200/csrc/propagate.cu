@@ -195,10 +195,7 @@ __device__ __forceinline__ void tile_accumulate(float (&acc)[T * T], const float
 #pragma unroll
             for (int j = 0; j < T; ++j) {
                 float s = acc[i * T + j];
-                s = exact_step(s, A[i].x, B[j].x);
-                s = exact_step(s, A[i].y, B[j].y);
-                s = exact_step(s, A[i].z, B[j].z);
-                s = exact_step(s, A[i].w, B[j].w);
+                s = exact_step4(s, A[i], B[j]);
                 acc[i * T + j] = s;
             }
     }

@@ -233,10 +233,7 @@ __global__ void __launch_bounds__(ID_WARPS * 32) init_dists_kernel(const float *
 #pragma unroll 8
                 for (int q = 0; q < nfull; ++q) {
                     const float4 x = mine[q], y = __ldg(b + q);
-                    acc = exact_step(acc, x.x, y.x);
-                    acc = exact_step(acc, x.y, y.y);
-                    acc = exact_step(acc, x.z, y.z);
-                    acc = exact_step(acc, x.w, y.w);
+                    acc = exact_step4(acc, x, y);
                 }
                 if (dim & 3) {  // the first dim % 4 columns of the last chunk (padding ignored)
                     const float4 x = mine[nfull], y = __ldg(b + nfull);

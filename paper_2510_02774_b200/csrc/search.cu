@@ -185,10 +185,7 @@ __global__ void __launch_bounds__(BF_TILE) bf_partial_kernel(const float *__rest
                 for (int q = 0; q < BF_QB; ++q) {
                     const float4 y = qv[q * nq4 + dc + c];
                     float s = acc[q];
-                    s = exact_step(s, y.x, x.x);
-                    s = exact_step(s, y.y, x.y);
-                    s = exact_step(s, y.z, x.z);
-                    s = exact_step(s, y.w, x.w);
+                    s = exact_step4(s, y, x);
                     acc[q] = s;
                 }
             }
@@ -306,10 +303,7 @@ __global__ void __launch_bounds__(GS_WARPS * 32) greedy_kernel(const int64_t *__
 #pragma unroll 4
         for (int c = 0; c < nq4; ++c) {
             const float4 a = __ldg(x + c), b = y[c];
-            s = exact_step(s, b.x, a.x);
-            s = exact_step(s, b.y, a.y);
-            s = exact_step(s, b.z, a.z);
-            s = exact_step(s, b.w, a.w);
+            s = exact_step4(s, b, a);
         }
         return s;
     };

@@ -469,10 +469,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                                                    : *reinterpret_cast<const float4 *>(stg + t3_off(ii, q));
                             const float4 y = MULTI ? __ldg(reinterpret_cast<const float4 *>(a.data + (int64_t)mt.ids[jj] * a.ld) + q)
                                                    : *reinterpret_cast<const float4 *>(stg + t3_off(jj, q));
-                            dx = exact_step(dx, x.x, y.x);
-                            dx = exact_step(dx, x.y, y.y);
-                            dx = exact_step(dx, x.z, y.z);
-                            dx = exact_step(dx, x.w, y.w);
+                            dx = exact_step4(dx, x, y);
                         }
                         const float nn = mt.nrm[i] + mt.nrm[jr];
                         const float err = fabsf(fmaf(-2.0f, __uint_as_float(r[c]), nn) - dx);
@@ -567,14 +564,8 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             for (int c = 0; c < nq; ++c) {
                 const int cn = c + 1 < nq ? c + 1 : c;
                 const float4 nx1 = ld(r0, q0, cn), ny1 = ld(r1, q1, cn), nx2 = ld(r2, q2, cn), ny2 = ld(r3, q3, cn);
-                s1 = exact_step(s1, x1.x, y1.x);
-                s2 = exact_step(s2, x2.x, y2.x);
-                s1 = exact_step(s1, x1.y, y1.y);
-                s2 = exact_step(s2, x2.y, y2.y);
-                s1 = exact_step(s1, x1.z, y1.z);
-                s2 = exact_step(s2, x2.z, y2.z);
-                s1 = exact_step(s1, x1.w, y1.w);
-                s2 = exact_step(s2, x2.w, y2.w);
+                s1 = exact_step4(s1, x1, y1);
+                s2 = exact_step4(s2, x2, y2);
                 x1 = nx1;
                 y1 = ny1;
                 x2 = nx2;
@@ -640,10 +631,8 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                         const int q = c * 32 + lane;
                         if (q < nq) {
                             const float4 x = __ldg(ra + q), y = __ldg(rb + q), z = __ldg(rc + q), w = __ldg(rd + q);
-                            p1 = make_float4(exact_step(0.f, x.x, y.x), exact_step(0.f, x.y, y.y), exact_step(0.f, x.z, y.z),
-                                             exact_step(0.f, x.w, y.w));
-                            p2 = make_float4(exact_step(0.f, z.x, w.x), exact_step(0.f, z.y, w.y), exact_step(0.f, z.z, w.z),
-                                             exact_step(0.f, z.w, w.w));
+                            p1 = sq4(x, y);
+                            p2 = sq4(z, w);
                         } else {
                             p1 = p2 = make_float4(0.f, 0.f, 0.f, 0.f);
                         }
@@ -724,10 +713,8 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                         const float4 y1 = *reinterpret_cast<const float4 *>(stg + t3_off(j1, lane));
                         const float4 x2 = *reinterpret_cast<const float4 *>(stg + t3_off(i2, lane));
                         const float4 y2 = *reinterpret_cast<const float4 *>(stg + t3_off(j2, lane));
-                        p1 = make_float4(exact_step(0.f, x1.x, y1.x), exact_step(0.f, x1.y, y1.y), exact_step(0.f, x1.z, y1.z),
-                                         exact_step(0.f, x1.w, y1.w));
-                        p2 = make_float4(exact_step(0.f, x2.x, y2.x), exact_step(0.f, x2.y, y2.y), exact_step(0.f, x2.z, y2.z),
-                                         exact_step(0.f, x2.w, y2.w));
+                        p1 = sq4(x1, y1);
+                        p2 = sq4(x2, y2);
                     }
                     {
                         float *ps = sm.psq + (E * 3 + ew) * S::PSQW;

@@ -255,10 +255,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_pairs_kernel(PropArgs a, int
         for (int c = 0; c < nq; ++c) {
             const float4 x = *reinterpret_cast<const float4 *>(stg + tc::stage_off(i, c));
             const float4 y = *reinterpret_cast<const float4 *>(stg + tc::stage_off(j, c));
-            s = exact_step(s, x.x, y.x);
-            s = exact_step(s, x.y, y.y);
-            s = exact_step(s, x.z, y.z);
-            s = exact_step(s, x.w, y.w);
+            s = exact_step4(s, x, y);
         }
         return s;
     };
@@ -271,14 +268,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) tc_pairs_kernel(PropArgs a, int
             const float4 y1 = *reinterpret_cast<const float4 *>(stg + tc::stage_off(j1, c));
             const float4 x2 = *reinterpret_cast<const float4 *>(stg + tc::stage_off(i2, c));
             const float4 y2 = *reinterpret_cast<const float4 *>(stg + tc::stage_off(j2, c));
-            s1 = exact_step(s1, x1.x, y1.x);
-            s2 = exact_step(s2, x2.x, y2.x);
-            s1 = exact_step(s1, x1.y, y1.y);
-            s2 = exact_step(s2, x2.y, y2.y);
-            s1 = exact_step(s1, x1.z, y1.z);
-            s2 = exact_step(s2, x2.z, y2.z);
-            s1 = exact_step(s1, x1.w, y1.w);
-            s2 = exact_step(s2, x2.w, y2.w);
+            s1 = exact_step4(s1, x1, y1);
+            s2 = exact_step4(s2, x2, y2);
         }
         d1 = s1;
         d2 = s2;
