@@ -77,7 +77,10 @@ struct T3Smem {
     // SZ (SZ - 1) / 2 pairs, so small slots never truncate a list
     static constexpr int CL = PAIR_LIST < SZ * (SZ - 1) / 2 ? PAIR_LIST : SZ * (SZ - 1) / 2;
     static constexpr int RS = 4 + 2 * CL;  // record stride (int32), a multiple of 4
-    static constexpr int QC = 512;   // filter candidates per group (overflow: exact sweep)
+    // filter candidates per group in shared memory (overflow: an exact sweep; MULTI: the rest
+    // spill to the CTA's global list, so a smaller queue leaves room for wider exact batches)
+    static constexpr int QC = MULTI ? 256 : 512;
+    static constexpr int CN = MULTI && SZ >= 32 ? 4 : 2;  // MULTI: pairs per warp-cooperative batch
     T3Meta meta[T3_NM];
     float2 ab[2][T3_ROWS];        // filter terms (A = -inf: always a candidate; B = -1: dead row)
     uint32_t livec[2][4];         // bit r: row r's B >= 0 (a column that can pair)
@@ -89,7 +92,7 @@ struct T3Smem {
     uint32_t q[2][QC];            // (row i << 8) | row j
     // per exact warp: the squared differences of two pairs (MULTI: one 128-dim chunk; the
     // second pair's row starts 132 floats in, so the two summing lanes read distinct banks)
-    static constexpr int PSQW = MULTI ? 2 * 132 : 2 * 128;
+    static constexpr int PSQW = MULTI ? CN * 132 : 2 * 128;
     alignas(16) float psq[6 * PSQW];
     uint64_t mfull[T3_NM], mempty[T3_NM], full[T3_NS], empty[T3_NS], accf[2], acce[2], qrdy[2], qemp[2], rfree[2];
     uint32_t tmem_base;
@@ -619,37 +622,43 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 // two pairs per warp (keys k1, k2: group rows (i << 8) | j): the lanes square
                 // 16-byte chunks of the four rows, 128 dims at a time (the next chunk's loads
                 // issued before this chunk's sums), lanes 0 / 1 add the squares in order
-                auto coop2 = [&](uint32_t k1, uint32_t k2, float &x1, float &x2) {
-                    auto row = [&](int r) {
-                        const int32_t id = mt.ids[r];
-                        return reinterpret_cast<const float4 *>(a.data + (int64_t)(id < 0 ? 0 : id) * a.ld);
-                    };
-                    const float4 *ra = row((int)(k1 >> 8)), *rb = row((int)(k1 & 255u));
-                    const float4 *rc = row((int)(k2 >> 8)), *rd = row((int)(k2 & 255u));
-                    float4 p1, p2;
+                // S::CN pairs per warp (key of pair p in lane p): every lane squares its 16-byte
+                // chunk of all pairs' rows (the next 128-dim chunk's loads issued before this
+                // chunk's sums); lane p adds pair p's squares in the reference's order
+                constexpr int CN = S::CN;
+                auto coopN = [&](uint32_t mykey, int np) -> float {
+                    int32_t ia[CN], ib[CN];
+#pragma unroll
+                    for (int p = 0; p < CN; ++p) {
+                        const uint32_t kk = __shfl_sync(FULL, mykey, p);
+                        const int32_t x = mt.ids[kk >> 8], y = mt.ids[kk & 255u];
+                        ia[p] = p < np && x >= 0 ? x : 0;
+                        ib[p] = p < np && y >= 0 ? y : 0;
+                    }
+                    float4 pv[CN];
                     auto sq = [&](int c) {
                         const int q = c * 32 + lane;
-                        if (q < nq) {
-                            const float4 x = __ldg(ra + q), y = __ldg(rb + q), z = __ldg(rc + q), w = __ldg(rd + q);
-                            p1 = sq4(x, y);
-                            p2 = sq4(z, w);
-                        } else {
-                            p1 = p2 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                        for (int p = 0; p < CN; ++p) {
+                            pv[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+                            if (p < np && q < nq)
+                                pv[p] = sq4(__ldg(reinterpret_cast<const float4 *>(a.data + (int64_t)ia[p] * a.ld) + q),
+                                            __ldg(reinterpret_cast<const float4 *>(a.data + (int64_t)ib[p] * a.ld) + q));
                         }
                     };
                     sq(0);
                     float acc = 0.0f;
                     for (int c = 0; c < nch; ++c) {
-                        reinterpret_cast<float4 *>(ps)[lane] = p1;
-                        reinterpret_cast<float4 *>(ps + 132)[lane] = p2;
+#pragma unroll
+                        for (int p = 0; p < CN; ++p) reinterpret_cast<float4 *>(ps + 132 * p)[lane] = pv[p];
                         __syncwarp();
                         if (c + 1 < nch) sq(c + 1);
-                        if (lane < 2) {
-                            const float4 *pv = reinterpret_cast<const float4 *>(ps + 132 * lane);
+                        if (lane < np) {
+                            const float4 *pr = reinterpret_cast<const float4 *>(ps + 132 * lane);
                             const int nc = nq - c * 32 < 32 ? nq - c * 32 : 32;
 #pragma unroll 8
                             for (int cc = 0; cc < nc; ++cc) {
-                                const float4 v = pv[cc];
+                                const float4 v = pr[cc];
                                 acc = __fadd_rn(acc, v.x);
                                 acc = __fadd_rn(acc, v.y);
                                 acc = __fadd_rn(acc, v.z);
@@ -658,8 +667,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                         }
                         __syncwarp();
                     }
-                    x1 = __shfl_sync(FULL, acc, 0);
-                    x2 = __shfl_sync(FULL, acc, 1);
+                    return acc;
                 };
                 auto keep = [&](uint32_t kk, float x) {
                     const int i = (int)(kk >> 8), j = (int)(kk & 255u);
@@ -670,15 +678,11 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 // overflow buffer (written by the filter before its qrdy arrival)
                 const uint32_t *gqb = a.w.t3q + ((int64_t)blockIdx.x * 2 + b) * T3Q_GROUP;
                 auto qkey = [&](int e) { return e < S::QC ? sm.q[b][e] : gqb[e - S::QC]; };
-                for (int e = ew * 2; e < qn; e += 6) {  // warp-uniform: queue entries e, e + 1
-                    const bool two = e + 1 < qn;
-                    const uint32_t k1 = qkey(e), k2 = two ? qkey(e + 1) : k1;
-                    float x1, x2;
-                    coop2(k1, k2, x1, x2);
-                    if (lane == 0) {
-                        keep(k1, x1);
-                        if (two) keep(k2, x2);
-                    }
+                for (int e0 = ew * CN; e0 < qn; e0 += 3 * CN) {  // warp-uniform
+                    const int np = qn - e0 < CN ? qn - e0 : CN;
+                    const uint32_t mykey = lane < np ? qkey(e0 + lane) : 0u;
+                    const float x = coopN(mykey, np);
+                    if (lane < np) keep(mykey, x);
                 }
                 tc::warp_arrive(&sm.qemp[b]);
                 if (et == 0) T3P_EV(g, 6);
