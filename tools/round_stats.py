@@ -7,7 +7,8 @@ import paper_2510_02774_b200 as g
 from paper_2510_02774_b200 import builder as B
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
 dim = int(sys.argv[2]) if len(sys.argv) > 2 else 128
-ds = g.generate(n, dim, "gaussian", seed=1)
+dist = sys.argv[3] if len(sys.argv) > 3 else "gaussian"
+ds = g.generate(n, dim, dist, seed=1)
 p = g.BuildParams(S=20, R=96, T1=4, T2=15, rho=0.6, seed=1)
 st = g.init_neighbors(ds, p)
 rows = torch.zeros((B.num_rounds(p), 20), dtype=torch.int64, device="cuda")
