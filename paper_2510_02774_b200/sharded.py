@@ -40,6 +40,7 @@ from . import _lib
 from .builder import (
     _ORDER_CODES,
     MASK64,
+    MSG_PER_ROW,
     STREAM_ROUND_BASE,
     RoundStats,
     _device,
@@ -52,6 +53,8 @@ from .builder import (
     effective_params,
     normalize_rows_,
     num_rounds,
+    optimistic_msg_capacity,
+    padded_ld,
     upload,
 )
 from .core import BuildParams, Dataset, Graph, validate_params
@@ -90,9 +93,12 @@ class ShardPools(_DevicePools):
 
     def __init__(self, data_dev, dim, cap, lo, hi, n_total, world, msg_capacity=None):
         rows = hi - lo
-        # outgoing <= sum(k) of owned rows; incoming is data dependent (hubs): 2x headroom.
-        # Overflow is detected on the device and raised (GRNND_ST_LOST), never truncated.
-        mc = msg_capacity if msg_capacity is not None else max(2 * rows * cap, 1024)
+        # send buffer and inbox: MSG_PER_ROW slots per owned row (the single-GPU build's
+        # optimistic capacity; C2's largest round needs ~20).  An emission beyond it is
+        # counted on the device (GRNND_ST_LOST); an inbox beyond it is seen by every rank
+        # in the counts exchange -- either way build_sharded redoes the build at the
+        # worst-case capacity, never on truncated messages.
+        mc = msg_capacity if msg_capacity is not None else max(optimistic_msg_capacity(rows, cap), 1024)
         super().__init__(data_dev, dim, cap, lo=lo, hi=hi, n_total=n_total, msg_capacity=mc)
         self.world = world
         p = self.struct()
@@ -119,19 +125,26 @@ class ShardPools(_DevicePools):
     @_on_device
     def apply(self, kind: int, n_in: int, stats: torch.Tensor) -> None:
         if n_in > self.msg_capacity:
-            raise DeviceError(f"rank receives {n_in} messages > capacity {self.msg_capacity}")
+            raise CapacityError(f"rank receives {n_in} messages > capacity {self.msg_capacity}")
         p = self.struct(stats)
         _lib.call("grnnd_round_apply", C.byref(p), kind, int(n_in), _stream(self.dev))
         self.swap()
 
 
+class CapacityError(DeviceError):
+    """A round needs more message slots than the workspace holds (raised on every rank)."""
+
+
 def exchange_all_to_all(out: torch.Tensor, send_counts: list[int], inb: torch.Tensor, group=None) -> int:
-    """The per-round exchange over torch.distributed (NCCL on GPUs, gloo on CPU): counts
-    all-to-all, then ONE all-to-all of the packed [m, MSG_WORDS] payload, received in
-    source-rank order into ``inb``.  Returns the number of messages received."""
+    """The per-round exchange over torch.distributed (NCCL on GPUs, gloo on CPU): ONE
+    all-gather of every rank's P send counts (so each rank sees every inbox size and an
+    over-full inbox anywhere stops all ranks together, before the payload moves), then
+    ONE all-to-all of the packed [m, MSG_WORDS] payload, received in source-rank order
+    into ``inb``.  Returns the number of messages received."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
     if out.is_cuda and dist.get_backend(group) == "gloo":
         # gloo's all-to-all moves host tensors: stage through the host (functional multi-rank
         # runs on one GPU, where NCCL refuses two ranks per device)
@@ -140,13 +153,17 @@ def exchange_all_to_all(out: torch.Tensor, send_counts: list[int], inb: torch.Te
         inb[:n_in].copy_(inb_h[:n_in])
         return n_in
     dev = out.device
-    sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
-    rc = torch.empty(world, dtype=torch.int64, device=dev)
-    dist.all_to_all_single(rc, sc, group=group)
-    recv_counts = [int(x) for x in rc.cpu().tolist()]
+    sc = torch.tensor(list(send_counts) + [inb.shape[0]], dtype=torch.int64, device=dev)
+    allc = torch.empty(world * (world + 1), dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(allc, sc, group=group)
+    m = allc.cpu().view(world, world + 1)  # [source, destination] counts + each rank's inbox capacity
+    recv_counts = [int(x) for x in m[:, rank].tolist()]
     n_out, n_in = sum(send_counts), sum(recv_counts)
-    if n_in > inb.shape[0]:
-        raise DeviceError(f"rank receives {n_in} messages > capacity {inb.shape[0]}")
+    inbox = m[:, :world].sum(0)
+    over = [r for r in range(world) if int(inbox[r]) > int(m[r, world])]
+    if over:
+        raise CapacityError(f"rank(s) {over} receive more messages than their inbox holds "
+                            f"({[int(inbox[r]) for r in over]} > {[int(m[r, world]) for r in over]})")
     dist.all_to_all_single(inb[:n_in], out[:n_out], output_split_sizes=recv_counts,
                            input_split_sizes=send_counts, group=group)
     return n_in
@@ -166,7 +183,8 @@ class ShardedBuild:
     """This rank's part of a sharded build."""
 
     def __init__(self, data_dev: torch.Tensor, dim: int, params: BuildParams, rank: int, world: int,
-                 pair_order: str = "disordered", group=None, msg_capacity=None, metric: str = "l2"):
+                 pair_order: str = "disordered", group=None, msg_capacity=None, metric: str = "l2",
+                 normalize_in_place: bool = False):
         n = int(data_dev.shape[0])
         self.params = effective_params(params, n)
         validate_params(self.params, n)
@@ -178,7 +196,12 @@ class ShardedBuild:
         self.metric, self.raw, self.dim = metric, data_dev, dim
         self.bounds = shard_bounds(n, world)
         self.bounds_dev = torch.tensor(self.bounds, dtype=torch.int64, device=data_dev.device)
-        work = torch.empty_like(data_dev) if metric == "ip" else data_dev
+        # IP works on L2-normalised rows: a working copy keeps the caller's rows for reruns;
+        # normalize_in_place (C5: no room for a second 38.4 GB copy) normalises them once
+        self.copy_rows = metric == "ip" and not normalize_in_place
+        if metric == "ip" and normalize_in_place:
+            normalize_rows_(data_dev, dim)
+        work = torch.empty_like(data_dev) if self.copy_rows else data_dev
         self.pools = ShardPools(work, dim, self.params.R, self.bounds[rank], self.bounds[rank + 1], n, world,
                                 msg_capacity)
         self.stats = torch.zeros((num_rounds(self.params), _lib.NSTATS), dtype=torch.int64, device=data_dev.device)
@@ -191,7 +214,7 @@ class ShardedBuild:
         p, pools = self.params, self.pools
         self.stats.zero_()
         self.kinds = []
-        if self.metric == "ip":
+        if self.copy_rows:
             pools.data.copy_(self.raw)
             normalize_rows_(pools.data, self.dim)
         pools.compute_norms()
@@ -239,6 +262,76 @@ class ShardedBuild:
         return [RoundStats.from_counters(k, c) for k, c in zip(self.kinds, rows)]
 
 
+def run_sharded(data_dev: torch.Tensor, dim: int, params: BuildParams, rank: int, world: int,
+                pair_order: str = "disordered", group=None, *, metric: str = "l2", exchange: Callable | None = None,
+                phase_events: list | None = None):
+    """This rank's build with the optimistic message capacity; if any rank's round
+    outgrows it (an emission the device counted as lost, or an over-full inbox seen in the
+    counts exchange) every rank redoes the build at the worst-case capacity -- the same
+    rule as the single-GPU build().  Returns (ShardedBuild, offsets, nbrs, bad, fail)."""
+    import torch.distributed as dist
+
+    for attempt in range(2):
+        mc = None if attempt == 0 else max(2 * (shard_bounds(int(data_dev.shape[0]), world)[rank + 1]
+                                                - shard_bounds(int(data_dev.shape[0]), world)[rank]) * params.R, 1024)
+        sb = ShardedBuild(data_dev, dim, params, rank, world, pair_order, group, msg_capacity=mc, metric=metric)
+        try:
+            offsets, nbrs, bad, fail = sb.run(phase_events, exchange)
+            lost = int(sb.stats[:, _lib.ST_LOST].sum().item())
+        except CapacityError:
+            if attempt:
+                raise
+            lost = 1
+        flag = torch.tensor([lost], dtype=torch.int64, device=data_dev.device)
+        if dist.is_initialized():
+            dist.all_reduce(flag, group=group)
+        if attempt == 0 and int(flag.item()):
+            del sb
+            continue
+        if int(flag.item()):
+            raise CapacityError("sharded build lost messages at the worst-case capacity")
+        return sb, offsets, nbrs, bad, fail
+
+
+def memory_plan(n: int, dim: int, R: int, world: int = 1, metric: str = "l2", *,
+                msg_per_row: int = MSG_PER_ROW, normalize_in_place: bool = False) -> dict:
+    """Per-rank device bytes of a sharded build (the largest shard): replicated vectors
+    (fp32 [N, ld]; IP keeps a normalised working copy next to the caller's rows unless the
+    caller normalises in place), the row norms of the tensor-core filter, the one pool
+    buffer of the owned rows, the workspace (grnnd_workspace_bytes: messages, pair records,
+    masks, staging) and the CSR emitted at the end.  SURVEY 8(d) C5: 100M x 96 at P=8."""
+    rows = max(hi - lo for lo, hi in zip(shard_bounds(n, world), shard_bounds(n, world)[1:]))
+    ld = padded_ld(dim)
+    mc = max(min(max(rows * R, 1), max(msg_per_row * rows, 1 << 16)), 1024)
+    plan = {
+        "vectors": n * ld * 4,
+        "vectors_ip_copy": n * ld * 4 if metric == "ip" and not normalize_in_place else 0,
+        "norms": n * 4,
+        "pools": rows * R * 8 + rows * 4,
+        "workspace": int(_lib.lib.grnnd_workspace_bytes(rows, R, mc)),
+        "csr": (rows + 1) * 8 + rows * R * 4,
+    }
+    plan["total"] = sum(plan.values())
+    plan.update(rows=rows, msg_capacity=mc)
+    return plan
+
+
+def generate_device(n: int, dim: int, seed: int = 1, device=None) -> torch.Tensor:
+    """Seeded standard-normal fp32 [n, ld] (zero-padded) generated on the device (torch's
+    counter-based Philox), for corpora with no host twin (C5: 38.4 GB); every rank that
+    calls it with the same arguments gets the same rows."""
+    dev = _device(device)
+    ld = padded_ld(dim)
+    out = torch.zeros((n, ld), dtype=torch.float32, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(int(seed))
+    chunk = max(1, (1 << 28) // ld)
+    for a in range(0, n, chunk):
+        b = min(n, a + chunk)
+        out[a:b, :dim].normal_(generator=gen)
+    return out
+
+
 def _gather_graph(parts, n: int, cap: int) -> Graph:
     offs, nbrs = [], []
     base = 0
@@ -269,8 +362,8 @@ def build_sharded(dataset: Dataset, params: BuildParams, pair_order: str = "diso
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     dev = _device(None)
     params, data_dev = _prepare(dataset, params, dev)
-    sb = ShardedBuild(data_dev, dataset.dim, params, rank, world, pair_order, group, metric=metric)
-    offsets, nbrs, bad, fail = sb.run()
+    sb, offsets, nbrs, bad, fail = run_sharded(data_dev, dataset.dim, params, rank, world, pair_order, group,
+                                               metric=metric)
     if int(fail.item()) or int(bad.item()):
         raise DeviceError("sharded build: init sampling failed or invalid graph")
     local_off = offsets.cpu().numpy()
@@ -297,7 +390,7 @@ def concat_exchange(shards: list[ShardedBuild]) -> list[int]:
         for r, src in enumerate(shards):
             a, b = int(offs[r][d]), int(offs[r][d + 1])
             if m + (b - a) > dst.pools.msg_capacity:
-                raise DeviceError(f"rank {d} receives more than {dst.pools.msg_capacity} messages")
+                raise CapacityError(f"rank {d} receives more than {dst.pools.msg_capacity} messages")
             dst.pools.inb[m: m + (b - a)].copy_(src.pools.out[a:b])
             m += b - a
         n_in.append(m)

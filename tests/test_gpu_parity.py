@@ -452,3 +452,76 @@ def test_split_tf32_filter_bit_exact(g, monkeypatch, dist, shift, R, mode):
     graph = g.build(g.Dataset(x), g.BuildParams(S=16, R=R, T1=2, T2=5, rho=0.6, seed=7))
     off, nb = oracle.build(x, 16, R, 2, 5, 0.6, 7)
     assert np.array_equal(graph.offsets, off) and np.array_equal(graph.neighbor_ids, nb)
+
+
+def _tied_pools(n, cap, seed):
+    """Duplicate-free pools with heavily tied distances (four values), random counts."""
+    rng = np.random.default_rng(seed)
+    ids = np.full((n, cap), -1, np.int32)
+    dists = np.zeros((n, cap), np.float32)
+    counts = rng.integers(0, cap + 1, n).astype(np.int32)
+    counts[:4] = [0, 1, cap, cap]
+    for v in range(n):
+        k = int(counts[v])
+        cand = rng.permutation(np.setdiff1d(np.arange(n), [v]))[:k]
+        ids[v, :k] = cand
+        dists[v, :k] = rng.integers(0, 4, k).astype(np.float32) * np.float32(0.25)
+    return ids, dists, counts
+
+
+@pytest.mark.parametrize("cap", [8, 33, 96, 130, 256])
+def test_reverse_selection_and_finalize_with_ties(K, g, cap):
+    """The warp bitonic (dist, id) sort of gen_reverse_messages (_numba_kernels.py:195-233)
+    and finalize_graph (builder.py:342-362) against the oracle on tie-heavy rows, every
+    keys-per-lane width (cap 8 ... 256)."""
+    n = 300
+    ids, dists, counts = _tied_pools(n, cap, cap)
+    for rho in (0.6, 1.0):
+        mt = np.full(n * cap, -7, np.int32)
+        mi = np.full(n * cap, -7, np.int32)
+        md = np.full(n * cap, -7.0, np.float32)
+        mc = np.zeros(n, np.int32)
+        K.gen_reverse_messages(ids, dists, counts, rho, mt, mi, md, mc)
+        wt, wi, wd, wc = oracle.gen_reverse_messages(ids, dists, counts, rho)
+        assert np.array_equal(mc, wc)
+        m = (np.arange(cap)[None, :] < mc[:, None]).ravel()
+        assert np.array_equal(mt[m], wt[m]) and np.array_equal(mi[m], wi[m])
+        assert np.array_equal(md[m].view(np.uint32), wd[m].view(np.uint32))
+    data = generate(n, 4, "gaussian", seed=1).data
+    st = g.BuildState.from_arrays(data, g.BuildParams(S=1, R=cap, T1=1, T2=1), ids, dists, counts)
+    graph = g.finalize_graph(st)
+    off, nb = oracle.finalize(ids, dists, counts)
+    assert np.array_equal(graph.offsets, off) and np.array_equal(graph.neighbor_ids, nb)
+
+
+@pytest.mark.parametrize("defect,msg", [("dup", "duplicate"), ("self", "self-loop"), ("range", "out of range")])
+def test_finalize_flags_invalid_rows_on_device(g, defect, msg):
+    """Graph.validate's checks (core.py:171-201) run inside the finalize kernel."""
+    n, cap = 200, 40
+    ids, dists, counts = _tied_pools(n, cap, 5)
+    v = 17
+    counts[v] = 30
+    ids[v, :30] = np.setdiff1d(np.arange(n), [v])[:30]
+    if defect == "dup":
+        ids[v, 29] = ids[v, 3]
+    elif defect == "self":
+        ids[v, 12] = v
+    else:
+        ids[v, 5] = n + 3
+    data = generate(n, 4, "gaussian", seed=1).data
+    st = g.BuildState.from_arrays(data, g.BuildParams(S=1, R=cap, T1=1, T2=1), ids, dists, counts)
+    with pytest.raises(g.ParamError, match=msg):
+        g.finalize_graph(st)
+
+
+@pytest.mark.parametrize("dim,cap", [(3, 40), (100, 96), (128, 130), (960, 33)])
+def test_init_dists_wide_rows_bit_exact(K, dim, cap):
+    """init_dists (_numba_kernels.py:118-122) with more than 32 neighbours per row (several
+    row groups) and partial 128-dim chunks."""
+    n = 500
+    data = generate(n, dim, "gaussian", seed=dim).data
+    rng = np.random.default_rng(cap)
+    ids = rng.integers(0, n, (n, cap)).astype(np.int32)
+    out = np.zeros((n, cap), np.float32)
+    K.init_dists(data, ids, out)
+    assert np.array_equal(out.view(np.uint32), oracle.init_dists(data, ids).view(np.uint32))

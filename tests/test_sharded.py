@@ -200,7 +200,7 @@ def test_message_overflow_is_reported():
         build_virtual_shards(ds, g.BuildParams(S=16, R=32, T1=2, T2=2, seed=1), 2, msg_capacity=2000)
 
 
-def _gpu_worker(rank, world, port, cfg, out_q):
+def _gpu_worker(rank, world, port, cfg, out_q, small_capacity=False):
     """One rank of a real multi-process sharded build on the GPU (ranks share cuda:0 over
     gloo: NCCL refuses two ranks on one device); the public build_sharded API."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -210,6 +210,10 @@ def _gpu_worker(rank, world, port, cfg, out_q):
         import paper_2510_02774_b200 as g
         from paper_2510_02774_b200.sharded import build_sharded
 
+        if small_capacity:  # every rank starts with 1024 message slots: forces the collective retry
+            import paper_2510_02774_b200.sharded as sh
+
+            sh.optimistic_msg_capacity = lambda rows, cap: 64
         n, dim, dist_name, S, R, T1, T2, seed = cfg
         ds = generate(n, dim, dist_name, seed=seed)
         log = []
@@ -221,17 +225,20 @@ def _gpu_worker(rank, world, port, cfg, out_q):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,cfg", [(2, (6000, 64, "gaussian", 16, 48, 2, 5, 3)),
-                                       (3, (4000, 32, "clustered", 12, 24, 2, 4, 5))])
-def test_multi_process_sharded_build_gpu_bit_exact(world, cfg):
+@pytest.mark.parametrize("world,cfg,small", [(2, (6000, 64, "gaussian", 16, 48, 2, 5, 3), False),
+                                             (3, (4000, 32, "clustered", 12, 24, 2, 4, 5), False),
+                                             (2, (5000, 32, "gaussian", 16, 32, 2, 3, 7), True)])
+def test_multi_process_sharded_build_gpu_bit_exact(world, cfg, small):
     """build_sharded in `world` separate processes (the exchange, the sharded pair phase and
-    apply, the graph gather): the oracle's graph and per-round redirect counts."""
+    apply, the graph gather): the oracle's graph and per-round redirect counts.  small: the
+    optimistic message capacity is overrun (emission and inbox), every rank redoes the
+    build at the worst-case capacity together, and the result is still exact."""
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, cfg, q)) for r in range(world)]
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, cfg, q, small)) for r in range(world)]
     for p in procs:
         p.start()
     off, nb, red = q.get(timeout=600)
@@ -243,3 +250,22 @@ def test_multi_process_sharded_build_gpu_bit_exact(world, cfg):
                                          with_stats=True)
     assert np.array_equal(off, want_off) and np.array_equal(nb, want_nb)
     assert red == st[:, 2].tolist()
+
+
+def test_c5_per_rank_memory_plan_fits_one_b200():
+    """SURVEY 8(d) C5 (100M x 96 over 8 B200, vectors replicated): a rank's device bytes --
+    vectors, norms, its pools, the workspace at the optimistic message capacity and the
+    final CSR -- fit in 180 GB (L2, and IP normalised in place); the worst-case message
+    capacity (the retry path) is what would not."""
+    from paper_2510_02774_b200.sharded import memory_plan
+
+    hbm = 180e9
+    for metric in ("l2", "ip"):
+        p = memory_plan(100_000_000, 96, 96, 8, metric, normalize_in_place=True)
+        assert p["rows"] == 12_500_000 and p["vectors"] == 100_000_000 * 96 * 4
+        assert p["total"] < hbm, (metric, p["total"])
+    worst = memory_plan(100_000_000, 96, 96, 8, msg_per_row=96)
+    assert worst["workspace"] > memory_plan(100_000_000, 96, 96, 8)["workspace"]
+    # C4 on one GPU (the bench config) and at P = 8
+    assert memory_plan(10_000_000, 96, 96, 1, "ip")["total"] < hbm
+    assert memory_plan(10_000_000, 96, 96, 8, "ip")["total"] < memory_plan(10_000_000, 96, 96, 1, "ip")["total"]
