@@ -344,6 +344,11 @@ def run_gpu(args, rank: int, world: int, local_rank: int):
     launches = (int(_lib.lib.grnnd_launch_count()) - launches0) // args.steps
     ms_step = e0.elapsed_time(e1) / args.steps
     ms_step = max_over_ranks(ms_step)
+    # one more (untimed) build with the instrumentation counters on (GRNND_ST_PAIRS_REF, the
+    # reference-semantics pair count of the roofline's compute term): the same graph and stats
+    _lib.lib.grnnd_set_instrumentation(1)
+    out = eng.run()
+    _lib.lib.grnnd_set_instrumentation(0)
     offsets, nbrs, bad, fail = out
     assert int(bad.item()) == 0, "finalize flagged an invalid graph"
     assert int(fail.item()) == 0, "initial sampling failed"

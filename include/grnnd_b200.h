@@ -80,6 +80,10 @@ const char *grnnd_last_error(void);
 int grnnd_abi_version(void);
 /* kernels launched by this library since load (host-side counter; for launch accounting) */
 unsigned long long grnnd_launch_count(void);
+/* costly instrumentation counters (GRNND_ST_PAIRS_REF: the reference-semantics pair count,
+   ~20% of the decide kernel's instructions) on / off for later launches; off by default
+   (the counter then stays 0).  Returns the previous setting. */
+int grnnd_set_instrumentation(int on);
 
 /* ------------------------------------------------------------------------ */
 /* (1) kernel-module entry points (device pointers)                          */

@@ -65,6 +65,7 @@ _SIGS = {
     "grnnd_last_error": (C.c_char_p, []),
     "grnnd_abi_version": (C.c_int, []),
     "grnnd_launch_count": (C.c_ulonglong, []),
+    "grnnd_set_instrumentation": (C.c_int, [C.c_int]),
     "grnnd_update_emit": (C.c_int, [C.POINTER(Pools), _u64, _u64, _i32, _vp]),
     "grnnd_reverse_emit": (C.c_int, [C.POINTER(Pools), _dbl, _vp]),
     "grnnd_apply_emitted": (C.c_int, [C.POINTER(Pools), _i32, _vp]),

@@ -21,6 +21,9 @@ static unsigned long long g_launches = 0;  // kernels this library launched (hos
 
 unsigned long long launch_count() { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
 
+static int g_instr = 0;  // costly instrumentation counters on (GRNND_ST_PAIRS_REF)
+int instrumentation() { return __atomic_load_n(&g_instr, __ATOMIC_RELAXED); }
+
 int current_device() {
     int d = 0;
     if (cudaGetDevice(&d) != cudaSuccess) return 0;
@@ -133,6 +136,11 @@ extern "C" {
 const char *grnnd_last_error(void) { return g_err; }
 int grnnd_abi_version(void) { return 1; }
 unsigned long long grnnd_launch_count(void) { return launch_count(); }
+int grnnd_set_instrumentation(int on) {
+    const int old = instrumentation();
+    __atomic_store_n(&g_instr, on ? 1 : 0, __ATOMIC_RELAXED);
+    return old;
+}
 
 int grnnd_hash4_batch(uint64_t seed, uint64_t stream, const uint64_t *v, const uint64_t *i, int64_t m, uint64_t *out,
                       grnnd_stream_t s) {

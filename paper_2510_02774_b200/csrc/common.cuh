@@ -106,6 +106,7 @@ namespace grnnd {
 void set_error(const char* fmt, ...);
 int check_launch(const char* what, int nkernels = 1);
 unsigned long long launch_count();
+int instrumentation();  // grnnd_set_instrumentation
 constexpr int MAX_DEVICES = 64;
 // SM count of the CUDA runtime's current device (cached per device)
 int device_sm_count();

@@ -272,9 +272,11 @@ __device__ __forceinline__ uint64_t bits_below(int f, int w) {  // bits of word 
 // local memory): every word is compared against x's word
 template <int MW>
 __device__ __forceinline__ bool mask_bit(const uint64_t (&m)[MW], int x) {
+    // (an unconditional AND-OR per word: a conditional select is turned back into an
+    // indexed -- local-memory -- load by the compiler)
     uint64_t w = 0ull;
 #pragma unroll
-    for (int i = 0; i < MW; ++i) w = (x >> 6) == i ? m[i] : w;
+    for (int i = 0; i < MW; ++i) w |= m[i] & (0ull - (uint64_t)((x >> 6) == i));
     return (w >> (x & 63)) & 1ull;
 }
 
@@ -305,7 +307,7 @@ struct DecideSmem {
 // words; dist_of(key, j, nm, found) looks message j's exact distance up (warp-collective);
 // missing ones are re-evaluated from global rows.  Emits to the message list (or the
 // reference's slices), tombstones read_ids, counts redirects and reference-semantics pairs.
-template <int MW, class MaskFn, class DistFn>
+template <int MW, bool REFP, class MaskFn, class DistFn>
 __device__ __forceinline__ void decide_pool(const PropArgs &a, int k, int64_t v, const int32_t *ids,
                                             const uint8_t *pos, int16_t *perm, int16_t *e_tgt, int16_t *e_id,
                                             uint16_t *e_key, MaskFn masks, DistFn dist_of,
@@ -339,7 +341,7 @@ __device__ __forceinline__ void decide_pool(const PropArgs &a, int k, int64_t v,
             const int xa = act ? x0 + __ffs(act) - 1 : x0 + 32;
             // live anchors in [cur, xa) have no live redirect partner: they visit every
             // live partner after them (reference-semantics pair count)
-            if (x >= cur && x < xa && mylive) {
+            if (REFP && x >= cur && x < xa && mylive) {
 #pragma unroll
                 for (int i = 0; i < MW; ++i) refp += __popcll(live[i] & bits_above(x, i));
             }
@@ -356,9 +358,10 @@ __device__ __forceinline__ void decide_pool(const PropArgs &a, int k, int64_t v,
 #pragma unroll
                 for (int i = 0; i < MW; ++i) {
                     em[i] = c[i] & live[i] & ~am[i] & bits_below(f, i);
-                    // partners visited: live, position in (xa, f] (or (xa, k) without a break)
-                    const uint64_t vis = live[i] & bits_above(xa, i) & (f < k ? bits_below(f + 1, i) : ~0ull);
-                    refp += __popcll(vis);
+                    if (REFP) {  // partners visited: live, position in (xa, f] (or (xa, k) without a break)
+                        const uint64_t vis = live[i] & bits_above(xa, i) & (f < k ? bits_below(f + 1, i) : ~0ull);
+                        refp += __popcll(vis);
+                    }
                 }
             }
             f = __shfl_sync(FULL, f, src);
@@ -395,8 +398,8 @@ __device__ __forceinline__ void decide_pool(const PropArgs &a, int k, int64_t v,
                 }
                 ++base;
 #pragma unroll
-                for (int i = 0; i < MW; ++i)
-                    if ((xa >> 6) == i) live[i] &= ~(1ull << (xa & 63));
+                for (int i = 0; i < MW; ++i)  // (unconditional per word: keeps live[] in registers)
+                    live[i] &= ~((1ull << (xa & 63)) & (0ull - (uint64_t)((xa >> 6) == i)));
             }
             nm = base;
             cur = xa + 1;
@@ -467,7 +470,9 @@ __device__ __forceinline__ void decide_pool(const PropArgs &a, int k, int64_t v,
     __syncwarp();
 }
 
-template <int MW>
+// REFP: count the reference-semantics pairs (GRNND_ST_PAIRS_REF, instrumentation only:
+// ~20% of the kernel's instructions; grnnd_set_instrumentation)
+template <int MW, bool REFP>
 __global__ void __launch_bounds__(dec_warps<MW>() * 32, 4) decide_kernel(PropArgs a) {
     __shared__ DecideSmem<MW> sm;
     const int lane = lane_id(), wib = threadIdx.x >> 5;
@@ -493,8 +498,10 @@ __global__ void __launch_bounds__(dec_warps<MW>() * 32, 4) decide_kernel(PropArg
                 kl = a.read_count[vl];
                 cl = kl >= 2 ? a.w.clcnt[vl] : 0;
             }
-            unsigned long long rp = (kl >= 2 && cl == 0) ? (unsigned long long)kl * (unsigned long long)(kl - 1) / 2ull : 0ull;
-            refp_total += warp_sum(rp) * (lane == 0 ? 1ull : 0ull);
+            if (REFP) {
+                unsigned long long rp = (kl >= 2 && cl == 0) ? (unsigned long long)kl * (unsigned long long)(kl - 1) / 2ull : 0ull;
+                refp_total += warp_sum(rp) * (lane == 0 ? 1ull : 0ull);
+            }
             todo = __ballot_sync(FULL, cl != 0 && cl != CL_DONE);
         }
         while (todo) {
@@ -560,10 +567,24 @@ __global__ void __launch_bounds__(dec_warps<MW>() * 32, 4) decide_kernel(PropArg
             if (j < 32) {  // first batch: scatter
                 for (int t = lane; t < nm; t += 32) e_d[t] = __int_as_float(0x7FFFFFFF);
                 __syncwarp();
-                for (int t = 0; t < nm; ++t) {
-                    const uint32_t et = ek[t];
-                    for (int h = lane; h < ncl; h += 32)
-                        if (((uint32_t)srec[h].x & 0xFFFFu) == et) e_d[t] = __int_as_float(srec[h].y);
+                // the emitted keys ek[0, nm) ascend ((anchor pos, partner pos): anchors in
+                // position order, each anchor's messages in partner order, its anchor-far
+                // message last and beyond them): each record finds its message by bisection
+#pragma unroll 1
+                for (int h = lane; h < ncl; h += 32) {
+                    const uint32_t kk = (uint32_t)srec[h].x & 0xFFFFu;
+                    int lo = 0, n = nm;
+#pragma unroll 1
+                    while (n > 0) {
+                        const int half = n >> 1;
+                        if ((uint32_t)ek[lo + half] < kk) {
+                            lo += half + 1;
+                            n -= half + 1;
+                        } else {
+                            n = half;
+                        }
+                    }
+                    if (lo < nm && (uint32_t)ek[lo] == kk) e_d[lo] = __int_as_float(srec[h].y);
                 }
                 __syncwarp();
             }
@@ -572,7 +593,7 @@ __global__ void __launch_bounds__(dec_warps<MW>() * 32, 4) decide_kernel(PropArg
             found = __float_as_int(d) != 0x7FFFFFFF;
             return d;
         };
-        decide_pool<MW>(a, k, v, ids, pos, sm.perm[wib], sm.e_tgt[wib], sm.e_id[wib], sm.e_key[wib], masks, dist_of,
+        decide_pool<MW, REFP>(a, k, v, ids, pos, sm.perm[wib], sm.e_tgt[wib], sm.e_id[wib], sm.e_key[wib], masks, dist_of,
                         red_total, refp_total);
         }
     }
@@ -764,11 +785,16 @@ int launch_propagate(const PropArgs &a, cudaStream_t st) {
         const int64_t blocks = std::min<int64_t>((n + warps - 1) / warps, (int64_t)device_sm_count() * 16);
         kern<<<(unsigned)std::max<int64_t>(1, blocks), warps * 32, 0, st>>>(a);
     };
-    switch (a.w.mw) {
-        case 1: dec(decide_kernel<1>, dec_warps<1>()); break;
-        case 2: dec(decide_kernel<2>, dec_warps<2>()); break;
-        case 3: dec(decide_kernel<3>, dec_warps<3>()); break;
-        case 4: dec(decide_kernel<4>, dec_warps<4>()); break;
+    const bool refp = instrumentation() != 0;
+    switch (a.w.mw * 2 + (refp ? 1 : 0)) {
+        case 2: dec(decide_kernel<1, false>, dec_warps<1>()); break;
+        case 3: dec(decide_kernel<1, true>, dec_warps<1>()); break;
+        case 4: dec(decide_kernel<2, false>, dec_warps<2>()); break;
+        case 5: dec(decide_kernel<2, true>, dec_warps<2>()); break;
+        case 6: dec(decide_kernel<3, false>, dec_warps<3>()); break;
+        case 7: dec(decide_kernel<3, true>, dec_warps<3>()); break;
+        case 8: dec(decide_kernel<4, false>, dec_warps<4>()); break;
+        case 9: dec(decide_kernel<4, true>, dec_warps<4>()); break;
         default: set_error("cap %d > %d unsupported", a.cap, GRNND_MAX_CAP); return GRNND_EUNSUPPORTED;
     }
     return check_launch("decide_kernel");
