@@ -694,9 +694,12 @@ static int launch_tc_pairs(const PropArgs &a, int bin, cudaStream_t st) {
     return check_launch("tc_pairs_kernel");
 }
 
+#ifndef GRNND_T3_FORCE_MULTI
+#define GRNND_T3_FORCE_MULTI 0  // 1: D <= 128 runs the MULTI pipeline too (stage freed by the MMA)
+#endif
 template <int SZ>
 static int launch_tc3_pairs(const PropArgs &a, int bin, cudaStream_t st) {
-    const bool multi = a.dim > 128;
+    const bool multi = a.dim > 128 || GRNND_T3_FORCE_MULTI;
     const bool split = !multi && a.split;
     if (multi && device_sm_count() > T3Q_CTAS) {
         set_error("tc3: %d SMs > %d overflow-queue slots", device_sm_count(), T3Q_CTAS);

@@ -51,6 +51,9 @@ constexpr int T3_PAD = GRNND_T3_PAD;
 #ifndef GRNND_T3_WARPS
 #define GRNND_T3_WARPS 20
 #endif
+#ifndef GRNND_T3_PREF
+#define GRNND_T3_PREF 0  // 1: the filter issues two 32-column TMEM loads before scanning either
+#endif
 #ifndef GRNND_T3_FSPLIT
 #define GRNND_T3_FSPLIT 0  // 1: warps 20..22 take half of the filter's Gram columns (23 warps)
 #endif
@@ -510,7 +513,32 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 scan16(r, cb, tr);
                 if (cb + 16 < hi) scan16(r + 16, cb + 16, tr);
             };
+            // both 32-column TMEM loads of a warp in flight before either is scanned
+            auto scan64 = [&](int ca, bool ta, int cb2, bool tb, int hi) {  // columns [ca, ca+32), [cb2, cb2+32)
+                uint32_t r0[32], r1[32];
+                const bool h0 = ca < hi, h1 = cb2 >= 0 && cb2 < hi;
+                if (h0) tc::tmem_ld32_nw(trow + (uint32_t)ca, r0);
+                if (h1) tc::tmem_ld32_nw(trow + (uint32_t)cb2, r1);
+                tc::tmem_wait_ld();
+                if (h0) {
+                    scan16(r0, ca, ta);
+                    if (ca + 16 < hi) scan16(r0 + 16, ca + 16, ta);
+                }
+                if (h1) {
+                    scan16(r1, cb2, tb);
+                    if (cb2 + 16 < hi) scan16(r1 + 16, cb2 + 16, tb);
+                }
+            };
             if (GRNND_T3_NOFILTER) {
+            } else if (GRNND_T3_PREF && !GRNND_T3_FSPLIT) {
+                if (GP == 1) {
+                    scan64(fw * 32, false, fw < 2 ? fw * 32 + 32 : 0, fw == 2, kcols);
+                } else {
+                    const int c_lo = ((fw * 32) / SZ) * SZ, c_hi = ((fw * 32 + 31) / SZ + 1) * SZ;
+                    const int start = ((c_lo >> 4) << 4) > fw * 32 ? ((c_lo >> 4) << 4) : fw * 32;
+#pragma unroll 1
+                    for (int cb = start; cb < c_hi; cb += 64) scan64(cb, false, cb + 32, false, c_hi);  // warp-uniform
+                }
             } else if (GP == 1) {
                 // upper-triangle 32x32 blocks (a, b'), a <= b' < 3, two per warp: (fw, fw) and
                 // (fw, fw+1); warp 2 takes (0, 2) as its transpose (rows 64.., columns 0..31)
