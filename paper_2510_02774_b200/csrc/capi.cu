@@ -3,10 +3,19 @@
 #include <cstdio>
 #include <cstring>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a profiler injects itself
+
 #include "common.cuh"
 #include "propagate.cuh"
 
 namespace grnnd {
+
+// NVTX range over one C-ABI call (per-stage ranges for nsys / ncu --nvtx)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+#define GRNND_RANGE(name) ::grnnd::NvtxRange grnnd_nvtx_range_(name)
 
 static thread_local char g_err[1024] = "";
 
@@ -313,6 +322,7 @@ static int pools_workspace(const grnnd_pools *p, Workspace *w) {
 }
 
 int grnnd_init_pools(const grnnd_pools *p, int32_t S_, uint64_t seed, int64_t *fail_flag, grnnd_stream_t s) {
+    GRNND_RANGE("grnnd_init_pools");
     Workspace w;
     GRNND_TRY(pools_workspace(p, &w));
     const int64_t n = p->hi - p->lo;
@@ -405,6 +415,7 @@ static int apply_phase(const grnnd_pools *p, const Workspace &w, int32_t kind, c
 
 int grnnd_update_round(const grnnd_pools *p, uint64_t seed, uint64_t stream_id, int32_t order_code,
                        grnnd_stream_t s) {
+    GRNND_RANGE("grnnd_update_round");
     Workspace w;
     GRNND_TRY(pools_workspace(p, &w));
     if (order_code != 0 && order_code != 1) {
@@ -417,6 +428,7 @@ int grnnd_update_round(const grnnd_pools *p, uint64_t seed, uint64_t stream_id, 
 }
 
 int grnnd_reverse_round(const grnnd_pools *p, double rho, grnnd_stream_t s) {
+    GRNND_RANGE("grnnd_reverse_round");
     Workspace w;
     GRNND_TRY(pools_workspace(p, &w));
     if (!(rho > 0.0 && rho <= 1.0)) {
@@ -430,6 +442,7 @@ int grnnd_reverse_round(const grnnd_pools *p, double rho, grnnd_stream_t s) {
 
 int grnnd_update_emit(const grnnd_pools *p, uint64_t seed, uint64_t stream_id, int32_t order_code,
                       grnnd_stream_t s) {
+    GRNND_RANGE("grnnd_update_emit");
     Workspace w;
     GRNND_TRY(pools_workspace(p, &w));
     if (order_code != 0 && order_code != 1) {
@@ -441,6 +454,7 @@ int grnnd_update_emit(const grnnd_pools *p, uint64_t seed, uint64_t stream_id, i
 }
 
 int grnnd_reverse_emit(const grnnd_pools *p, double rho, grnnd_stream_t s) {
+    GRNND_RANGE("grnnd_reverse_emit");
     Workspace w;
     GRNND_TRY(pools_workspace(p, &w));
     if (!(rho > 0.0 && rho <= 1.0)) {
@@ -452,6 +466,7 @@ int grnnd_reverse_emit(const grnnd_pools *p, double rho, grnnd_stream_t s) {
 }
 
 int grnnd_apply_emitted(const grnnd_pools *p, int32_t kind, grnnd_stream_t s) {
+    GRNND_RANGE("grnnd_apply_emitted");
     Workspace w;
     GRNND_TRY(pools_workspace(p, &w));
     return apply_phase(p, w, kind, w.ctr + C_LIST, p->msg_capacity, S(s));
@@ -460,6 +475,7 @@ int grnnd_apply_emitted(const grnnd_pools *p, int32_t kind, grnnd_stream_t s) {
 int grnnd_round_emit(const grnnd_pools *p, int32_t kind, uint64_t seed, uint64_t stream_id, int32_t order_code,
                      double rho, const int64_t *rank_bounds, int32_t nranks, int64_t *send_counts,
                      grnnd_stream_t s) {
+    GRNND_RANGE("grnnd_round_emit");
     Workspace w;
     GRNND_TRY(pools_workspace(p, &w));
     GRNND_CUDA(cudaMemsetAsync(w.ctr + C_LIST, 0, sizeof(unsigned long long), S(s)));
@@ -477,6 +493,7 @@ int grnnd_round_buffers(const grnnd_pools *p, int32_t **out_pack, int32_t **in_p
 }
 
 int grnnd_round_apply(const grnnd_pools *p, int32_t kind, int64_t n_incoming, grnnd_stream_t s) {
+    GRNND_RANGE("grnnd_round_apply");
     Workspace w;
     GRNND_TRY(pools_workspace(p, &w));
     if (n_incoming < 0 || n_incoming > p->msg_capacity) {
@@ -503,6 +520,7 @@ int grnnd_finalize(const int32_t *ids, const float *dists, const int32_t *counts
 
 int grnnd_finalize_pools(const grnnd_pools *p, int64_t *offsets, int32_t *nbrs, int64_t *bad_flag,
                          grnnd_stream_t s) {
+    GRNND_RANGE("grnnd_finalize_pools");
     Workspace w;
     GRNND_TRY(pools_workspace(p, &w));
     const int64_t n = p->hi - p->lo;
