@@ -3,7 +3,7 @@
 #   gpu tests + smoke; C2 bench (+ the reference arm); the bench's ncu launch list and the
 #   per-round table; one ncu --set full capture of a steady round's pair phase (round 21,
 #   tc3 + stage + decide) -> <tag>_pair_phase_ncu.json; bench lines for C1, C2c, C3, C4;
-#   compute-sanitizer passes over a small build.
+#   (sanitizers: tools/sanitize.sh, run separately where compute-sanitizer is allowed).
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 TAG=${TAG:-full}
@@ -27,5 +27,5 @@ timeout 600 python bench.py --config c1 --steps 5 --warmup 3 > gpurun_out/${TAG}
 timeout 900 python bench.py --config c2c --no-cpu --steps 3 --warmup 3 > gpurun_out/${TAG}_c2c_bench.log 2>&1
 timeout 1200 python bench.py --config c3 --no-cpu --steps 2 --warmup 3 > gpurun_out/${TAG}_c3_bench.log 2>&1
 timeout 1500 python bench.py --config c4 --no-cpu --steps 2 --warmup 3 > gpurun_out/${TAG}_c4_bench.log 2>&1
-bash tools/sanitize.sh ${TAG} > /dev/null 2>&1
+# (compute-sanitizer passes: tools/sanitize.sh -- closed on this pool since r2cj; last results profiles/r2bp_sanitizers.txt)
 echo done
