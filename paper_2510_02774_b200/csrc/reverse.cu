@@ -44,55 +44,72 @@ __device__ __forceinline__ void row_ranks(const int32_t (&id)[RPL], const float 
 
 template <int RPL>
 __global__ void __launch_bounds__(256) reverse_select_kernel(ReverseArgs a) {
+    // warp per vertex, 32 consecutive vertices per warp step: their message counts are known
+    // from the pool sizes alone, so one list reservation (atomicAdd) covers all 32
     const int lane = lane_id();
     const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long attempts = 0;
-    for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < a.n; v += warps) {
-        const int k = a.read_count[v];
-        const int64_t vg = a.lo + v;
-        if (k == 0) {
-            if (a.slice_mode && lane == 0) a.msg_cnt[v] = 0;
-            continue;
-        }
-        int32_t id[RPL];
-        float d[RPL];
-        int rank[RPL];
+    for (int64_t v0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; v0 < a.n; v0 += warps * 32) {
+        const int kl = v0 + lane < a.n ? a.read_count[v0 + lane] : 0;
+        const int ml = kl > 0 ? reverse_count(a.rho, kl) : 0;
+        int incl = ml;  // inclusive warp scan of the counts
 #pragma unroll
-        for (int r = 0; r < RPL; ++r) {
-            const int s = r * 32 + lane;
-            id[r] = s < k ? a.read_ids[v * a.cap + s] : TOMB;
-            d[r] = s < k ? a.read_dists[v * a.cap + s] : 0.0f;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += t;
         }
-        row_ranks<RPL>(id, d, k, rank);
-        const int m = reverse_count(a.rho, k);
-        attempts += (unsigned long long)m;
-        unsigned long long base = 0;
+        unsigned long long wbase = 0;
         if (!a.slice_mode) {
-            if (lane == 0) base = atomicAdd(&a.w.ctr[C_LIST], (unsigned long long)m);
-            base = __shfl_sync(FULL, base, 0);
+            if (lane == 31 && incl > 0) wbase = atomicAdd(&a.w.ctr[C_LIST], (unsigned long long)incl);
+            wbase = __shfl_sync(FULL, wbase, 31);
         }
+        const int excl = incl - ml;
+        const int tot = __shfl_sync(FULL, incl, 31);  // (every lane: a full-mask shuffle)
+        attempts += lane == 0 ? (unsigned long long)tot : 0ull;
+        const int nv = a.n - v0 < 32 ? (int)(a.n - v0) : 32;
+        for (int j = 0; j < nv; ++j) {
+            const int64_t v = v0 + j;
+            const int k = __shfl_sync(FULL, kl, j);
+            const int m = __shfl_sync(FULL, ml, j);
+            const unsigned long long base = wbase + (unsigned long long)__shfl_sync(FULL, excl, j);
+            const int64_t vg = a.lo + v;
+            if (k == 0) {
+                if (a.slice_mode && lane == 0) a.msg_cnt[v] = 0;
+                continue;
+            }
+            int32_t id[RPL];
+            float d[RPL];
+            int rank[RPL];
 #pragma unroll
-        for (int r = 0; r < RPL; ++r) {
-            const int s = r * 32 + lane;
-            if (s < k && rank[r] < m) {
-                if (a.slice_mode) {
-                    a.msg_tgt[v * a.cap + rank[r]] = id[r];
-                    a.msg_id[v * a.cap + rank[r]] = (int32_t)vg;
-                    a.msg_dist[v * a.cap + rank[r]] = d[r];
-                } else {
-                    const unsigned long long p = base + (unsigned long long)rank[r];
-                    if (p < (unsigned long long)a.w.msg_capacity) {
-                        a.w.e_key[p] = vg * a.cap + rank[r];
-                        a.w.e_tgt[p] = id[r];
-                        a.w.e_id[p] = (int32_t)vg;
-                        a.w.e_dist[p] = d[r];
+            for (int r = 0; r < RPL; ++r) {
+                const int s = r * 32 + lane;
+                id[r] = s < k ? a.read_ids[v * a.cap + s] : TOMB;
+                d[r] = s < k ? a.read_dists[v * a.cap + s] : 0.0f;
+            }
+            row_ranks<RPL>(id, d, k, rank);
+#pragma unroll
+            for (int r = 0; r < RPL; ++r) {
+                const int s = r * 32 + lane;
+                if (s < k && rank[r] < m) {
+                    if (a.slice_mode) {
+                        a.msg_tgt[v * a.cap + rank[r]] = id[r];
+                        a.msg_id[v * a.cap + rank[r]] = (int32_t)vg;
+                        a.msg_dist[v * a.cap + rank[r]] = d[r];
                     } else {
-                        a.w.ctr[C_OVERFLOW] = 1ull;
+                        const unsigned long long p = base + (unsigned long long)rank[r];
+                        if (p < (unsigned long long)a.w.msg_capacity) {
+                            a.w.e_key[p] = vg * a.cap + rank[r];
+                            a.w.e_tgt[p] = id[r];
+                            a.w.e_id[p] = (int32_t)vg;
+                            a.w.e_dist[p] = d[r];
+                        } else {
+                            a.w.ctr[C_OVERFLOW] = 1ull;
+                        }
                     }
                 }
             }
+            if (a.slice_mode && lane == 0) a.msg_cnt[v] = m;
         }
-        if (a.slice_mode && lane == 0) a.msg_cnt[v] = m;
     }
     if (lane == 0 && a.stats && attempts) {
         atomicAdd((unsigned long long *)&a.stats[GRNND_ST_REVERSE_ATTEMPTS], attempts);
@@ -131,7 +148,7 @@ static unsigned warp_grid(int64_t n) {
 
 int launch_reverse_select(const ReverseArgs &a, cudaStream_t st) {
     if (a.n <= 0) return GRNND_OK;
-    const unsigned g = warp_grid(a.n);
+    const unsigned g = warp_grid((a.n + 31) / 32);  // a warp step covers 32 vertices
     switch ((a.cap + 31) / 32) {
         case 1: reverse_select_kernel<1><<<g, 256, 0, st>>>(a); break;
         case 2: reverse_select_kernel<2><<<g, 256, 0, st>>>(a); break;
