@@ -200,12 +200,15 @@ def test_message_overflow_is_reported():
         build_virtual_shards(ds, g.BuildParams(S=16, R=32, T1=2, T2=2, seed=1), 2, msg_capacity=2000)
 
 
-def _gpu_worker(rank, world, port, cfg, out_q, small_capacity=False):
+def _gpu_worker(rank, world, port, cfg, out_q, small_capacity=False, backend="gloo"):
     """One rank of a real multi-process sharded build on the GPU (ranks share cuda:0 over
     gloo: NCCL refuses two ranks on one device); the public build_sharded API."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2510_02774_b200 as g
         from paper_2510_02774_b200.sharded import build_sharded
@@ -269,3 +272,26 @@ def test_c5_per_rank_memory_plan_fits_one_b200():
     # C4 on one GPU (the bench config) and at P = 8
     assert memory_plan(10_000_000, 96, 96, 1, "ip")["total"] < hbm
     assert memory_plan(10_000_000, 96, 96, 8, "ip")["total"] < memory_plan(10_000_000, 96, 96, 1, "ip")["total"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("small", [False, True])
+def test_nccl_exchange_single_rank_gpu_bit_exact(small):
+    """The NCCL code path of build_sharded (all_gather_into_tensor of the counts, all_to_all_single
+    of the packed payload, device buffers) in a one-rank NCCL group on cuda:0 -- the collectives
+    the 8-GPU build issues; small: through the collective capacity retry."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    cfg = (5000, 48, "gaussian", 16, 40, 2, 4, 11)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_gpu_worker, args=(0, 1, _free_port(), cfg, q, small, "nccl"))
+    p.start()
+    off, nb, red = q.get(timeout=600)
+    p.join(timeout=120)
+    assert p.exitcode == 0
+    n, dim, dist_name, S, R, T1, T2, seed = cfg
+    want_off, want_nb, st = oracle.build(generate(n, dim, dist_name, seed=seed).data, S, R, T1, T2, 0.6, seed,
+                                         with_stats=True)
+    assert np.array_equal(off, want_off) and np.array_equal(nb, want_nb)
+    assert red == st[:, 2].tolist()
