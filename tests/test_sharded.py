@@ -295,3 +295,36 @@ def test_nccl_exchange_single_rank_gpu_bit_exact(small):
                                          with_stats=True)
     assert np.array_equal(off, want_off) and np.array_equal(nb, want_nb)
     assert red == st[:, 2].tolist()
+
+
+@pytest.mark.gpu
+def test_memory_plan_matches_device_allocation():
+    """sharded.memory_plan against what a rank actually allocates (the C5 probe's accounting
+    at a size one test can afford): device-generated corpus, one rank of four, init + the
+    round-1 pair phase + the final CSR buffers.  Peak within 2% of the plan."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2510_02774_b200 as g
+    from paper_2510_02774_b200.builder import _finalize_device
+    from paper_2510_02774_b200.sharded import ShardedBuild, generate_device, memory_plan
+
+    n, dim, world = 400_000, 96, 4
+    params = g.BuildParams(S=20, R=96, T1=4, T2=15, rho=0.6, seed=1)
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    base = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    data = generate_device(n, dim, seed=1, device="cuda:0")
+    again = generate_device(1000, dim, seed=1, device="cuda:0")
+    assert torch.equal(again, generate_device(1000, dim, seed=1, device="cuda:0"))  # seeded
+    del again
+    sb = ShardedBuild(data, dim, params, 1, world, metric="ip", normalize_in_place=True)
+    gen = sb.rounds()
+    next(gen)  # init + round-1 emit
+    offsets, nbrs, bad = _finalize_device(sb.pools)
+    torch.cuda.synchronize()
+    peak = torch.cuda.max_memory_allocated() - base
+    plan = memory_plan(n, dim, params.R, world, "ip", normalize_in_place=True)
+    assert abs(peak - plan["total"]) <= 0.02 * plan["total"], (peak, plan)
+    norms = data[:, :dim].norm(dim=1)
+    assert torch.allclose(norms, torch.ones_like(norms), atol=1e-5)  # IP rows normalised in place
