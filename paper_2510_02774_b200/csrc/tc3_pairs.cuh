@@ -51,6 +51,9 @@ constexpr int T3_PAD = GRNND_T3_PAD;
 #ifndef GRNND_T3_WARPS
 #define GRNND_T3_WARPS 20
 #endif
+#ifndef GRNND_T3_EXACT1
+#define GRNND_T3_EXACT1 1  // a thread with one queued pair runs one chain (not the pair twice)
+#endif
 #ifndef GRNND_T3_PREF
 #define GRNND_T3_PREF 0  // 1: the filter issues two 32-column TMEM loads before scanning either
 #endif
@@ -580,6 +583,27 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
         constexpr int NE = 96;
         // two chains per thread, the next chunk's four 16-byte loads issued before this chunk's
         // sums (the shared-memory latency is otherwise exposed once per chunk)
+        // one chain (a thread without a second pair: the chains are shared-memory bound --
+        // random rows hit the same 16-byte bank groups -- so a duplicated second chain is not free)
+        auto exact1 = [&](const unsigned char *stg, int i1, int j1) -> float {
+            const uint32_t r0 = (uint32_t)((i1 >> 3) * 1024 + (i1 & 7) * 128), q0 = (uint32_t)(i1 & 7);
+            const uint32_t r1 = (uint32_t)((j1 >> 3) * 1024 + (j1 & 7) * 128), q1 = (uint32_t)(j1 & 7);
+            auto ld = [&](uint32_t rb, uint32_t rq, int c) {
+                return *reinterpret_cast<const float4 *>(stg + (uint32_t)(c >> 3) * T3_KB + rb +
+                                                         ((((uint32_t)c & 7u) ^ rq) << 4));
+            };
+            float s1 = 0.0f;
+            float4 x1 = ld(r0, q0, 0), y1 = ld(r1, q1, 0);
+#pragma unroll 4
+            for (int c = 0; c < nq; ++c) {
+                const int cn = c + 1 < nq ? c + 1 : c;
+                const float4 nx1 = ld(r0, q0, cn), ny1 = ld(r1, q1, cn);
+                s1 = exact_step4(s1, x1, y1);
+                x1 = nx1;
+                y1 = ny1;
+            }
+            return s1;
+        };
         auto exact2 = [&](const unsigned char *stg, int i1, int j1, int i2, int j2, float &d1, float &d2) {
             const uint32_t r0 = (uint32_t)((i1 >> 3) * 1024 + (i1 & 7) * 128), q0 = (uint32_t)(i1 & 7);
             const uint32_t r1 = (uint32_t)((j1 >> 3) * 1024 + (j1 & 7) * 128), q1 = (uint32_t)(j1 & 7);
@@ -779,8 +803,9 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                     const bool two = e + NE < qn;
                     const uint32_t k1 = qk[t], k2 = two ? qk[t + 1] : k1;
                     const int i1 = (int)(k1 >> 8), j1 = (int)(k1 & 255u), i2 = (int)(k2 >> 8), j2 = (int)(k2 & 255u);
-                    float x1, x2;
-                    exact2(stg, i1, j1, i2, j2, x1, x2);
+                    float x1, x2 = 0.0f;
+                    if (GRNND_T3_EXACT1 && !two) x1 = exact1(stg, i1, j1);
+                    else exact2(stg, i1, j1, i2, j2, x1, x2);
                     const float a1 = mt.dv[i1], b1 = mt.dv[j1];
                     if (x1 < (a1 >= b1 ? a1 : b1)) record(i1, j1, x1);
                     const float a2 = mt.dv[i2], b2 = mt.dv[j2];
