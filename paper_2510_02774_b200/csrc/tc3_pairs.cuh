@@ -767,17 +767,19 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                     if (lane < nq) {
                         const float4 x1 = *reinterpret_cast<const float4 *>(stg + t3_off(i1, lane));
                         const float4 y1 = *reinterpret_cast<const float4 *>(stg + t3_off(j1, lane));
-                        const float4 x2 = *reinterpret_cast<const float4 *>(stg + t3_off(i2, lane));
-                        const float4 y2 = *reinterpret_cast<const float4 *>(stg + t3_off(j2, lane));
                         p1 = sq4(x1, y1);
-                        p2 = sq4(x2, y2);
+                        if (two) {  // (warp-uniform; no second pair: no second pair of row reads)
+                            const float4 x2 = *reinterpret_cast<const float4 *>(stg + t3_off(i2, lane));
+                            const float4 y2 = *reinterpret_cast<const float4 *>(stg + t3_off(j2, lane));
+                            p2 = sq4(x2, y2);
+                        }
                     }
                     {
                         float *ps = sm.psq + (E * 3 + ew) * S::PSQW;
                         reinterpret_cast<float4 *>(ps)[lane] = p1;
-                        reinterpret_cast<float4 *>(ps + 128)[lane] = p2;
+                        if (two) reinterpret_cast<float4 *>(ps + 128)[lane] = p2;
                         __syncwarp();
-                        if (lane < 2) {  // lane 0: pair 1, lane 1: pair 2; the reference's order
+                        if (lane < (two ? 2 : 1)) {  // lane 0: pair 1, lane 1: pair 2; the reference's order
                             const float4 *pv = reinterpret_cast<const float4 *>(ps + 128 * lane);
                             float sx = 0.0f;
 #pragma unroll 8
@@ -824,8 +826,9 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                         if (two) tile_decode(t + NE, s2, u2);
                         const int i1 = pp * SZ + s1, j1 = pp * SZ + u1 + 1;
                         const int i2 = two ? pp * SZ + s2 : i1, j2 = two ? pp * SZ + u2 + 1 : j1;
-                        float x1, x2;
-                        exact2(stg, i1, j1, i2, j2, x1, x2);
+                        float x1, x2 = 0.0f;
+                        if (GRNND_T3_EXACT1 && !two) x1 = exact1(stg, i1, j1);
+                        else exact2(stg, i1, j1, i2, j2, x1, x2);
                         const float a1 = mt.dv[i1], b1 = mt.dv[j1];
                         if (mt.ids[i1] != TOMB && mt.ids[j1] != TOMB && x1 < (a1 >= b1 ? a1 : b1)) record(i1, j1, x1);
                         const float a2 = mt.dv[i2], b2 = mt.dv[j2];
