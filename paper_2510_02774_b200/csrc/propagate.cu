@@ -712,7 +712,7 @@ static int launch_tc3_pairs(const PropArgs &a, int bin, cudaStream_t st) {
                                     (multi ? sizeof(T3Smem<SZ, true>) : sizeof(T3Smem<SZ, false>)) + 1024;
     static SmemOptIn optin[3];  // one per kernel
     GRNND_CUDA(optin[multi ? 1 : split ? 2 : 0].ensure(kern, smem));
-    kern<<<device_sm_count(), T3_NT, smem, st>>>(a, bin);
+    kern<<<device_sm_count(), multi ? T3Cfg<true>::NT : T3Cfg<false>::NT, smem, st>>>(a, bin);
     return check_launch("tc3_pairs_kernel");
 }
 

@@ -18,7 +18,8 @@
 //                size: tools/ubench_gather*.cu);
 //   warp 1       MMA: one thread fences the async proxy and issues the 16 MMAs of group g
 //                into TMEM accumulator g % 2;
-//   warps 4-6    filter (TMEM lanes 0..95): Gram -> band candidates -> queue g % 2;
+//   warps 4-6    filter (TMEM lanes 0..95): Gram -> band candidates -> queue g % 2; warps
+//                20-22 (FSPLIT, default) scan the other half of the Gram's column blocks;
 //   warps 2,3,7 / 8,9,10  two exact sets (even / odd groups): exact chains of the queue ->
 //                redirect records -> global (bulk stores); release the stage and meta slot.
 // Groups: 96 rows = one pool of k <= 96, or 96/SZ pools of k <= SZ (SZ = 8, 16, 24, 32, 48).
@@ -41,7 +42,7 @@ constexpr float TC_EPS_SPLIT = 3.0517578125e-05f;  // 2^-15 (~3x th
 #define GRNND_T3_PAD 0
 #endif
 #ifndef GRNND_T3_WCOOP
-#define GRNND_T3_WCOOP 16
+#define GRNND_T3_WCOOP 8
 #endif
 constexpr int T3_WCOOP = GRNND_T3_WCOOP;  // queues up to this length: warp-cooperative chains (<= 32)
 constexpr int T3_NM = GRNND_T3_NM;    // metadata slots
@@ -49,7 +50,7 @@ constexpr int T3_NM = GRNND_T3_NM;    // metadata slots
 // those are bytes of T3Smem (> 4 KB), read into accumulator rows 96..127 that nothing uses
 constexpr int T3_PAD = GRNND_T3_PAD;
 #ifndef GRNND_T3_WARPS
-#define GRNND_T3_WARPS 20
+#define GRNND_T3_WARPS 23
 #endif
 #ifndef GRNND_T3_EXACT1
 #define GRNND_T3_EXACT1 1  // a thread with one queued pair runs one chain (not the pair twice)
@@ -58,12 +59,19 @@ constexpr int T3_PAD = GRNND_T3_PAD;
 #define GRNND_T3_PREF 0  // 1: the filter issues two 32-column TMEM loads before scanning either
 #endif
 #ifndef GRNND_T3_FSPLIT
-#define GRNND_T3_FSPLIT 0  // 1: warps 20..22 take half of the filter's Gram columns (23 warps)
+#define GRNND_T3_FSPLIT 1  // 1: warps 20..22 take half of the filter's Gram columns (23 warps)
 #endif
-constexpr int T3_NT = 32 * GRNND_T3_WARPS;
-constexpr int T3_NP = GRNND_T3_WARPS - 11 - 3 * GRNND_T3_FSPLIT;  // row producers (11..)
-constexpr int T3_NF = 96 * (1 + GRNND_T3_FSPLIT);                  // filter threads
-static_assert(!GRNND_T3_FSPLIT || (11 + T3_NP) % 4 == 0, "filter warps must map to TMEM lane quarters 0..2");
+// warp layout per pipeline: D <= 128 runs the split filter (23 warps); MULTI (D > 128) keeps
+// one filter set and 20 warps (its register budget: measured 1.45 vs 1.53 s at C3)
+template <bool MULTI>
+struct T3Cfg {
+    static constexpr int WARPS = MULTI ? 20 : GRNND_T3_WARPS;
+    static constexpr int FSPLIT = MULTI ? 0 : GRNND_T3_FSPLIT;
+    static constexpr int NT = 32 * WARPS;
+    static constexpr int NP = WARPS - 11 - 3 * FSPLIT;  // row producers (warps 11..)
+    static constexpr int NF = 96 * (1 + FSPLIT);         // filter threads
+    static_assert(!FSPLIT || (11 + NP) % 4 == 0, "filter warps must map to TMEM lane quarters 0..2");
+};
 
 struct alignas(16) T3Meta {  // one group's metadata (staged by tc_stage_kernel, one bulk copy)
     int32_t ids[T3_ROWS];
@@ -167,7 +175,9 @@ __device__ long long g_t3trace[64][10];  // CTA 0: per group event times (profil
 // each stage with tcgen05.commit (the exact sets never hold a stage); the exact chains read
 // the candidate pairs' rows from global memory (L2: the group's rows were just streamed).
 template <int SZ, bool MULTI, bool SPLIT>
-__global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin) {
+__global__ void __launch_bounds__(T3Cfg<MULTI>::NT, 1) tc3_pairs_kernel(PropArgs a, int bin) {
+    using CF = T3Cfg<MULTI>;
+    constexpr int T3_NT = CF::NT, T3_NP = CF::NP, T3_NF = CF::NF;
     using S = T3Smem<SZ, MULTI>;
     constexpr int GP = S::GP;
     constexpr int R = T3_ROWS;
@@ -377,7 +387,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
             }
         }
         __syncwarp();
-    } else if ((warp >= 4 && warp <= 6) || (warp >= 11 + T3_NP && warp < 11 + T3_NP + 3 * GRNND_T3_FSPLIT)) {
+    } else if ((warp >= 4 && warp <= 6) || (warp >= 11 + T3_NP && warp < 11 + T3_NP + 3 * CF::FSPLIT)) {
         // ================= filter (TMEM lanes 0..95) =================
         // warps 4..6 (and with FSPLIT 20..22: the same TMEM lanes, the other column blocks)
         const bool fb = warp >= 11 + T3_NP;
@@ -533,7 +543,7 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 }
             };
             if (GRNND_T3_NOFILTER) {
-            } else if (GRNND_T3_PREF && !GRNND_T3_FSPLIT) {
+            } else if (GRNND_T3_PREF && !CF::FSPLIT) {
                 if (GP == 1) {
                     scan64(fw * 32, false, fw < 2 ? fw * 32 + 32 : 0, fw == 2, kcols);
                 } else {
@@ -547,20 +557,20 @@ __global__ void __launch_bounds__(T3_NT, 1) tc3_pairs_kernel(PropArgs a, int bin
                 // (fw, fw+1); warp 2 takes (0, 2) as its transpose (rows 64.., columns 0..31)
                 const int c0 = fw * 32, c1 = fw < 2 ? fw * 32 + 32 : 0;
                 const bool t1 = fw == 2;
-#if GRNND_T3_FSPLIT
-                const int cb = fb ? c1 : c0;
-                if (cb < kcols) scan32(cb, kcols, fb && t1);
-#else
+                if constexpr (CF::FSPLIT) {
+                    const int cb = fb ? c1 : c0;
+                    if (cb < kcols) scan32(cb, kcols, fb && t1);
+                } else {
 #pragma unroll 1
-                for (int h = 0; h < 2; ++h) {  // warp-uniform
-                    const int cb = h ? c1 : c0;
-                    if (cb < kcols) scan32(cb, kcols, h && t1);
+                    for (int h = 0; h < 2; ++h) {  // warp-uniform
+                        const int cb = h ? c1 : c0;
+                        if (cb < kcols) scan32(cb, kcols, h && t1);
+                    }
                 }
-#endif
             } else {
                 const int c_lo = ((fw * 32) / SZ) * SZ, c_hi = ((fw * 32 + 31) / SZ + 1) * SZ;
                 const int start = ((c_lo >> 4) << 4) > fw * 32 ? ((c_lo >> 4) << 4) : fw * 32;
-                constexpr int CSTEP = 32 * (1 + GRNND_T3_FSPLIT);
+                constexpr int CSTEP = 32 * (1 + CF::FSPLIT);
 #pragma unroll 1
                 for (int cb = start + (fb ? 32 : 0); cb < c_hi; cb += CSTEP) scan32(cb, c_hi, false);  // warp-uniform
             }
